@@ -1,0 +1,351 @@
+"""LUT-layer throughput on B200 — BASELINE.json metric on configs[4].
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--table f32|i8] [--k 16|64]
+    python bench.py --impl reference ...   # the reference's CPU path (oracle port), all host cores
+
+Workload (BASELINE.json configs[4], the scaling sweep): one LUT Linear layer,
+N = 2^20 rows per GPU (weak scaling: rows sharded across ranks, tables
+replicated, no collective), D = M = 4096, V = 32 -> C = 128, K = 16 (or 64),
+inputs ~N(0,1), centroids ~N(0,1), weights ~N(0, 1/D), fp32 or int8 tables.
+A step = encode + lookup-aggregate over the rank's N rows, input resident in
+HBM.  Inputs (17.2 GB) are far larger than L2 (126 MB), so no L2 flush is
+needed between steps.  Rank 0 prints ONE JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LUT-layer rows/sec and effective GOP/s at 1/2/4/8 B200; % of binding roofline"
+UNIT = "rows/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--table", choices=["f32", "i8"], default="f32")
+    p.add_argument("--k", type=int, default=16)
+    p.add_argument("--rows", type=int, default=1 << 20, help="rows per GPU")
+    p.add_argument("--dim", type=int, default=4096)
+    p.add_argument("--v", type=int, default=32)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--cpu-rows", type=int, default=0, help="CPU sample rows per core (0 = default)")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), float(pk.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+# ------------------------------------------------------------- CPU side
+
+
+_CPU_WORK = None  # set before the fork pool starts; workers inherit it (no pickling in the timed loop)
+
+
+def _cpu_worker(_i):
+    from oracle import lut_oracle as O
+
+    a, books, table, q, scale, integer = _CPU_WORK
+    if integer:
+        return O.lut_layer_infer(a, books, q=q, scale=scale).shape[0]
+    return O.lut_layer_infer(a, books, table=table, integer=False).shape[0]
+
+
+def cpu_reference(dim, m, v, k, integer, rows_per_core, steps, warmup, seed=7):
+    """The reference's CPU path (oracle port of lutkit.kernels.lut_layer_infer,
+    encode in f64 + ascending-c gather) on all host cores, rows sharded over
+    a process pool (one BLAS thread per process, as the reference caps it)."""
+    import multiprocessing as mp
+
+    from oracle import lut_oracle as O
+
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OMP_NUM_THREADS"] = "1"
+    cores = len(os.sched_getaffinity(0))
+    rng = O.make_rng(seed)
+    c = dim // v
+    books = rng.standard_normal((c, k, v)).astype(np.float32)
+    w = (rng.standard_normal((dim, m)) / np.sqrt(dim)).astype(np.float32)
+    table = O.build_table(w, books)
+    q, scale = O.quantize_table(table) if integer else (None, None)
+    shard = rng.standard_normal((rows_per_core, dim)).astype(np.float32)
+    global _CPU_WORK
+    _CPU_WORK = (shard, books, table, q, scale, integer)
+    ctx = mp.get_context("fork")
+    times = []
+    with ctx.Pool(cores) as pool:
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            done = sum(pool.map(_cpu_worker, range(cores), chunksize=1))
+            assert done == rows_per_core * cores
+            dt = time.perf_counter() - t0
+            if i >= warmup:
+                times.append(dt)
+    rows = rows_per_core * cores
+    med = statistics.median(times)
+    return {"value": rows / med, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{rows} rows ({rows_per_core}/core) of the same layer, median of {len(times)} steps; "
+                      f"oracle port of lutkit lut_layer_infer ({'int8' if integer else 'f32'} tables)",
+            "seconds_per_step": med, "rows": rows}
+
+
+# ------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            names = {
+                "hw_slowdown": getattr(N, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+                "hw_thermal_slowdown": getattr(N, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                "sw_thermal_slowdown": getattr(N, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                "sw_power_cap": getattr(N, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
+            }
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                        r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                        for nm, bit in names.items():
+                            if r & bit:
+                                self.reasons.add(nm)
+                    except Exception:
+                        pass
+                    self._stop.wait(0.1)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception:
+            self._t = None
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(1.0)
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------- GPU side
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    integer = args.table == "i8"
+    m = d = args.dim
+    v, k = args.v, args.k
+    c = d // v
+    config = {"workload": "BASELINE configs[4]: single LUT Linear, scaling sweep",
+              "rows_per_gpu": args.rows, "d": d, "m": m, "v": v, "c": c, "k": k, "table": args.table,
+              "parallelism": f"row-sharded x{world}, tables replicated",
+              "l2": "inputs (4*N*D B) >> 126 MB L2; no flush needed"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        ref = cpu_reference(d, m, v, k, integer, rows_per_core=args.cpu_rows or (4096 if integer else 2048),
+                            steps=max(1, args.steps), warmup=max(0, min(args.warmup, 1)))
+        eff = 2.0 * d * m * ref["value"] / 1e9
+        line = {"impl": "reference", "metric": METRIC, "value": ref["value"], "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ref["seconds_per_step"] * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+                "data": "synthetic", "config": config, "effective_gops": eff,
+                "cpu_baseline": {k_: ref[k_] for k_ in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": ref["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_reference(d, m, v, k, integer, rows_per_core=args.cpu_rows or (4096 if integer else 2048),
+                            steps=2, warmup=1)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2302_03213_b200 as L
+    from paper_2302_03213_b200 import _device as D
+    from paper_2302_03213_b200._lib import check, load
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = load()
+
+    # ---- layer (replicated) and this rank's rows (generated on device from (seed, rank))
+    g = torch.Generator(device=dev).manual_seed(1234)
+    books = torch.randn((c, k, v), generator=g, device=dev)
+    w = torch.randn((d, m), generator=g, device=dev) / math.sqrt(d)
+    layer = L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=books, weight=w, qat=integer)
+    n = args.rows
+    ga = torch.Generator(device=dev).manual_seed(99 + rank)
+    a = torch.randn((n, d), generator=ga, device=dev)
+    codes = torch.empty((n, c), dtype=torch.uint8, device=dev)
+    out = torch.empty((n, m), dtype=torch.float32, device=dev)
+    near = torch.zeros(1, dtype=torch.int32, device=dev)
+    scales = layer.qtable.scales_tensor(dev) if integer else None
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        check(lib.lut_encode_f32(a.data_ptr(), n, d, layer.books_prep.data_ptr(), c, k, v, codes.data_ptr(), 8,
+                                 near.data_ptr(), sp))
+        if ev:
+            ev[1].record(stream)
+        if integer:
+            check(lib.lut_gather_i8(codes.data_ptr(), 8, n, c, k, m, layer.qtable.q.data_ptr(), scales.data_ptr(),
+                                    0, None, 0, out.data_ptr(), None, 0, None, sp))
+        else:
+            check(lib.lut_gather_f32(codes.data_ptr(), 8, n, c, k, m, layer.table.data_ptr(), None, 0,
+                                     out.data_ptr(), 0, None, sp))
+        if ev:
+            ev[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    near.zero_()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end)
+    enc_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    gat_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    rows_total = n * world
+    value = rows_total / (ms_step / 1e3)
+    eff_gops = 2.0 * d * m * value / 1e9
+    near_ties = int(near.item())
+
+    # ---- roofline of the dominant kernel (algorithmic bytes per launch / event time)
+    hbm_peak, sm_mhz_max, peak_kind = peaks()
+    s = 1 if integer else 4
+    gather_bytes = n * c + s * c * k * m + 4 * n * m
+    encode_bytes = 4 * n * d + n * c + 4 * c * k * v
+    lookups = n * m * c
+    smem_peak = 148 * 128 * sm_mhz_max * 1e6  # B/s, LDS bandwidth at max clock
+    if gat_ms >= enc_ms:
+        dom, dom_ms, dom_bytes = "gather", gat_ms, gather_bytes
+    else:
+        dom, dom_ms, dom_bytes = "encode", enc_ms, encode_bytes
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    layer_hbm = 4 * n * d + s * c * k * m + 4 * c * k * v + 4 * n * m
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None, "kernel": dom, "peak_kind": peak_kind,
+                "kernel_ms": {"encode": enc_ms, "gather": gat_ms},
+                "smem_lookup": {"bytes": lookups * s, "achieved_TBps": lookups * s / (gat_ms / 1e3) / 1e12,
+                                "peak_TBps": smem_peak / 1e12,
+                                "frac": (lookups * s / (gat_ms / 1e3)) / smem_peak},
+                "layer_hbm_floor_ms": layer_hbm / (hbm_peak * 1e9) * 1e3,
+                "layer_frac_of_hbm_floor": (layer_hbm / (hbm_peak * 1e9) * 1e3) / ms_step}
+
+    # ---- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        a_h = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
+        a_h.copy_(a)
+        o_h = torch.empty((n, m), dtype=torch.float32, pin_memory=True)
+        a_np, o_np = a_h.numpy(), o_h.numpy()
+        L.lut_layer_infer(a_np[: 1 << 14], layer, integer=integer)  # warm the executor
+        if world > 1:
+            dist.barrier()
+        times = []
+        for i in range(args.e2e_steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            L.lut_layer_infer(a_np, layer, integer=integer, out=o_np)
+            t1 = time.perf_counter()
+            if i:
+                times.append(t1 - t0)
+        e2e_s = statistics.median(times)
+        if world > 1:
+            t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        ok = bool(torch.equal(o_h[:4096].to(dev), out[:4096]))
+        e2e = {"value": rows_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * n * d,
+               "d2h_bytes_per_step": 4 * n * m, "steps": len(times), "matches_device_path": ok,
+               "api": "paper_2302_03213_b200.lut_layer_infer(numpy pinned) -> lut_pipeline_run"}
+        del a_h, o_h
+
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if not integer else "f32-encode/int8-table/int32-acc",
+            "data": "synthetic (seeded torch.randn on device; random-init centroids/weights)",
+            "config": config, "effective_gops": eff_gops, "near_ties": near_ties,
+            "near_tie_rate": near_ties / (n * c * args.steps),
+            "roofline": roofline, "clocks": clocks.summary(), "gpu_launches": 2 * args.steps,
+            "e2e": e2e, "cpu_baseline": None}
+    if cpu is not None:
+        line["cpu_baseline"] = {k_: cpu[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

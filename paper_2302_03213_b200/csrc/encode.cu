@@ -1,0 +1,588 @@
+// Nearest-centroid encode on sm_100a.
+//
+// Semantics: indices identical to the reference's encode_hard
+// (lutkit/pq.py:171-174; literal f64 squared distances, ties -> lowest k),
+// which centroid_search_fast (lutkit/kernels.py:62-102) reproduces with the
+// expansion ||p||^2 - 2 a.p.
+//
+// Arithmetic: fp32 FFMA evaluates d_k = ||p_k||^2 - 2 a.p_k (two interleaved
+// chains, the -2 folded exactly into a), tracking best and second-best.  The
+// fp32 error of any d_k is < 2(V+3) u (||a||^2 + max_k ||p_k||^2), u = 2^-24
+// (||p||^2 exact to 1 ulp, 2|a.p| <= ||a||^2 + ||p||^2).  If the gap between the
+// best and second-best fp32 distance is within TAU = 4(V+4) u (||a||^2 + pmax)
+// — twice the sum of the two bounds — the fp32 winner may differ from the
+// exact one, so that (row, codebook) is re-decided from literal f64
+// differences exactly like encode_hard, and counted as a near tie.  Outside
+// the bound the fp32 winner is provably the exact argmin.
+//
+// Kernels
+//  encode_tma_kernel<V>   V in {4, 8, 16, 32}: persistent, warp-specialised.
+//    One producer warp streams 32-column x 512-row tiles of A with TMA
+//    (cp.async.bulk.tensor, 128B swizzle) plus the prepared codebooks of those
+//    columns (cp.async.bulk) into a 3-stage mbarrier ring; 8 consumer warps,
+//    2 rows per lane, read their row's sub-vector conflict-free from the
+//    swizzled tile and the centroids as warp-broadcast LDS.128.  Codes are
+//    packed in registers and stored as 16-byte vectors per row group.
+//  encode_rows_kernel<VT> generic (any V <= 256, any K <= 256), one thread per
+//    (row, codebook-pair), templated row loader: dense rows or on-the-fly
+//    im2col patches from an NCHW batch (conv fusion, tensor.py:36-79).
+
+#include <float.h>
+
+#include "common.cuh"
+
+namespace lutgpu {
+
+
+__global__ void prepare_books_kernel(const float* __restrict__ books, int C, int K, int V,
+                                     float* __restrict__ prep) {
+  const int c = blockIdx.x;
+  const int S = prep_stride(K, V);
+  float* rec = prep + (size_t)c * S;
+  const float* src = books + (size_t)c * K * V;
+  for (int i = threadIdx.x; i < K * V; i += blockDim.x) rec[i] = src[i];
+  __shared__ float smax[32];
+  float local = 0.0f;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < V; ++j) {
+      double x = (double)src[k * V + j];
+      s = fma(x, x, s);
+    }
+    float f = (float)s;
+    rec[K * V + k] = f;
+    local = fmaxf(local, f);
+  }
+  for (int o = 16; o > 0; o >>= 1) local = fmaxf(local, __shfl_xor_sync(0xffffffffu, local, o));
+  if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = 0.0f;
+    for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) m = fmaxf(m, smax[w]);
+    rec[K * V + K] = m;
+    for (int i = K * V + K + 1; i < S; ++i) rec[i] = 0.0f;
+  }
+}
+
+__device__ __forceinline__ float tau_coef(int v) { return (4.0f * v + 16.0f) * 5.9604645e-8f; }
+
+// Literal f64 re-decision (encode_hard semantics) for one (row, codebook).
+template <class GetA>
+__device__ __noinline__ int exact_argmin(GetA get_a, const float* __restrict__ cent, int K, int V) {
+  double best = 0.0;
+  int bi = 0;
+  for (int k = 0; k < K; ++k) {
+    double s = 0.0;
+    for (int j = 0; j < V; ++j) {
+      double diff = (double)get_a(j) - (double)cent[k * V + j];
+      s = __dadd_rn(s, __dmul_rn(diff, diff));
+    }
+    if (k == 0 || s < best) {
+      best = s;
+      bi = k;
+    }
+  }
+  return bi;
+}
+
+// --------------------------------------------------------------- TMA path
+
+constexpr int kEncWarps = 8;                  // consumer warps
+constexpr int kEncThreads = (kEncWarps + 1) * 32;
+constexpr int kBoxRows = 256;                 // TMA box rows
+constexpr int kRPL = 2;                       // rows per lane
+constexpr int kTileRows = kBoxRows * kRPL;    // 512
+constexpr int kBoxBytes = kBoxRows * 128;     // 32 KB (32 f32 columns)
+
+struct EncTmaParams {
+  const float* prep;
+  int S;          // prepared record stride (floats)
+  int64_t n;
+  int C, K;
+  int G;          // codebooks per output group (flush granularity)
+  int ngroups;
+  int64_t ntiles;
+  uint8_t* codes;
+  int code_bits;
+  int64_t code_stride;  // bytes per row of codes
+  int* near_tie;
+  int stages;
+  int stage_bytes;
+};
+
+__device__ __forceinline__ void store_code_group(uint8_t* dst, uint32_t w0, uint32_t w1,
+                                                 uint32_t w2, uint32_t w3, int nbytes) {
+  if (nbytes == 16 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+    *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
+    return;
+  }
+  if (nbytes == 8 && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) {
+    *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
+    return;
+  }
+  if (nbytes == 4 && ((reinterpret_cast<uintptr_t>(dst) & 3) == 0)) {
+    *reinterpret_cast<uint32_t*>(dst) = w0;
+    return;
+  }
+  uint32_t w[4] = {w0, w1, w2, w3};
+  for (int i = 0; i < nbytes; ++i) dst[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+}
+
+template <int V>
+__global__ void __launch_bounds__(kEncThreads, 1)
+    encode_tma_kernel(const __grid_constant__ CUtensorMap tmap, const EncTmaParams p) {
+  constexpr int NB = 32 / V;   // codebooks per 32-column box
+  constexpr int NJ = V / 4;    // 16-byte chunks per sub-vector
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * p.stage_bytes);
+  uint64_t* empty = full + p.stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kEncWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int64_t nunits = p.ntiles * p.ngroups;
+  const int boxes_per_group = p.G / NB;
+  const int nboxes = (p.C + NB - 1) / NB;
+
+  if (warp == kEncWarps) {
+    // ---------------- producer
+    if (lane == 0) {
+      prefetch_tmap(&tmap);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int64_t tile = u / p.ngroups;
+        const int grp = (int)(u % p.ngroups);
+        const int b0 = grp * boxes_per_group;
+        const int b1 = min(nboxes, b0 + boxes_per_group);
+        for (int b = b0; b < b1; ++b) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + (size_t)stage * p.stage_bytes;
+          const int nsub = min(NB, p.C - b * NB);
+          const uint32_t book_bytes = (uint32_t)nsub * p.S * 4;
+          mbar_arrive_expect_tx(&full[stage], kRPL * kBoxBytes + book_bytes);
+#pragma unroll
+          for (int r = 0; r < kRPL; ++r)
+            tma_load_2d(st + r * kBoxBytes, &tmap, b * 32, (int32_t)(tile * kTileRows + r * kBoxRows),
+                        &full[stage]);
+          bulk_load(st + kRPL * kBoxBytes, p.prep + (size_t)b * NB * p.S, book_bytes, &full[stage]);
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  int stage = 0;
+  uint32_t phase = 0;
+  const int rr = warp * 32 + lane;  // row within each 256-row box
+  const int sw = rr & 7;            // 128B swizzle phase of this row
+  const float tau_c = tau_coef(V);
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t tile = u / p.ngroups;
+    const int grp = (int)(u % p.ngroups);
+    const int c_begin = grp * p.G;
+    const int c_end = min(p.C, c_begin + p.G);
+    const int b0 = c_begin / NB;
+    const int b1 = (c_end + NB - 1) / NB;
+    uint32_t pk[kRPL][4];
+#pragma unroll
+    for (int r = 0; r < kRPL; ++r) pk[r][0] = pk[r][1] = pk[r][2] = pk[r][3] = 0u;
+    int ncodes = 0;
+
+    for (int b = b0; b < b1; ++b) {
+      mbar_wait(&full[stage], phase);
+      const uint8_t* st = smem + (size_t)stage * p.stage_bytes;
+      const float* cent_all = reinterpret_cast<const float*>(st + kRPL * kBoxBytes);
+#pragma unroll
+      for (int sb = 0; sb < NB; ++sb) {
+        const int c = b * NB + sb;
+        if (c >= c_end) break;
+        const float* cb = cent_all + sb * p.S;
+        float a[kRPL][V];
+        float asq[kRPL];
+#pragma unroll
+        for (int r = 0; r < kRPL; ++r) {
+          const float* rowp = reinterpret_cast<const float*>(st + r * kBoxBytes + rr * 128);
+          asq[r] = 0.0f;
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) {
+            const float4 x = *reinterpret_cast<const float4*>(rowp + (((sb * NJ + j) ^ sw) << 2));
+            asq[r] = fmaf(x.x, x.x, asq[r]);
+            asq[r] = fmaf(x.y, x.y, asq[r]);
+            asq[r] = fmaf(x.z, x.z, asq[r]);
+            asq[r] = fmaf(x.w, x.w, asq[r]);
+            a[r][4 * j + 0] = -2.0f * x.x;
+            a[r][4 * j + 1] = -2.0f * x.y;
+            a[r][4 * j + 2] = -2.0f * x.z;
+            a[r][4 * j + 3] = -2.0f * x.w;
+          }
+        }
+        float best[kRPL], second[kRPL];
+        int bi[kRPL];
+#pragma unroll
+        for (int r = 0; r < kRPL; ++r) {
+          best[r] = FLT_MAX;
+          second[r] = FLT_MAX;
+          bi[r] = 0;
+        }
+        const float* norms = cb + p.K * V;
+#pragma unroll 2
+        for (int k = 0; k < p.K; ++k) {
+          const float* pk4 = cb + k * V;
+          const float pn = norms[k];
+          float acc0[kRPL], acc1[kRPL];
+#pragma unroll
+          for (int r = 0; r < kRPL; ++r) {
+            acc0[r] = pn;
+            acc1[r] = 0.0f;
+          }
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) {
+            const float4 q = *reinterpret_cast<const float4*>(pk4 + 4 * j);
+#pragma unroll
+            for (int r = 0; r < kRPL; ++r) {
+              float& acc = (j & 1) ? acc1[r] : acc0[r];
+              acc = fmaf(a[r][4 * j + 0], q.x, acc);
+              acc = fmaf(a[r][4 * j + 1], q.y, acc);
+              acc = fmaf(a[r][4 * j + 2], q.z, acc);
+              acc = fmaf(a[r][4 * j + 3], q.w, acc);
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < kRPL; ++r) {
+            const float d = acc0[r] + acc1[r];
+            second[r] = fminf(second[r], fmaxf(best[r], d));
+            bi[r] = (d < best[r]) ? k : bi[r];
+            best[r] = fminf(best[r], d);
+          }
+        }
+        const float pmax = norms[p.K];
+#pragma unroll
+        for (int r = 0; r < kRPL; ++r) {
+          const float tau = tau_c * (asq[r] + pmax);
+          if (!(second[r] - best[r] > tau)) {
+            // near tie (or NaN): exact f64 decision from the staged tile
+            const float* rowp = reinterpret_cast<const float*>(st + r * kBoxBytes + rr * 128);
+            auto get_a = [&](int j) {
+              const int q = sb * NJ + (j >> 2);
+              return rowp[((q ^ sw) << 2) + (j & 3)];
+            };
+            bi[r] = exact_argmin(get_a, cb, p.K, V);
+            const int64_t row = tile * kTileRows + r * kBoxRows + rr;
+            if (p.near_tie && row < p.n) atomicAdd(p.near_tie, 1);
+          }
+          // shift the code into the 128-bit per-row register
+          const uint32_t code = (uint32_t)bi[r];
+          if (p.code_bits == 8) {
+            pk[r][0] = __funnelshift_r(pk[r][0], pk[r][1], 8);
+            pk[r][1] = __funnelshift_r(pk[r][1], pk[r][2], 8);
+            pk[r][2] = __funnelshift_r(pk[r][2], pk[r][3], 8);
+            pk[r][3] = (pk[r][3] >> 8) | (code << 24);
+          } else {
+            pk[r][0] = __funnelshift_r(pk[r][0], pk[r][1], 4);
+            pk[r][1] = __funnelshift_r(pk[r][1], pk[r][2], 4);
+            pk[r][2] = __funnelshift_r(pk[r][2], pk[r][3], 4);
+            pk[r][3] = (pk[r][3] >> 4) | (code << 28);
+          }
+        }
+        ++ncodes;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == p.stages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+
+    // flush this group's codes: right-align the shift register first
+    const int bits = p.code_bits;
+    const int slots = 128 / bits;
+    for (int s = ncodes; s < slots; ++s) {
+#pragma unroll
+      for (int r = 0; r < kRPL; ++r) {
+        pk[r][0] = __funnelshift_r(pk[r][0], pk[r][1], bits);
+        pk[r][1] = __funnelshift_r(pk[r][1], pk[r][2], bits);
+        pk[r][2] = __funnelshift_r(pk[r][2], pk[r][3], bits);
+        pk[r][3] = pk[r][3] >> bits;
+      }
+    }
+    const int nbytes = (ncodes * bits + 7) / 8;
+    const int64_t off = (int64_t)c_begin * bits / 8;
+#pragma unroll
+    for (int r = 0; r < kRPL; ++r) {
+      const int64_t row = tile * kTileRows + r * kBoxRows + rr;
+      if (row < p.n)
+        store_code_group(p.codes + row * p.code_stride + off, pk[r][0], pk[r][1], pk[r][2], pk[r][3],
+                         nbytes);
+    }
+  }
+}
+
+// ------------------------------------------------------------ generic path
+
+struct DenseRows {
+  const float* a;
+  int64_t lda;
+  __device__ __forceinline__ float operator()(int64_t row, int col) const {
+    return __ldg(a + row * lda + col);
+  }
+};
+
+struct ConvRows {  // im2col on the fly; col = (ci, dy, dx) channel-major
+  const float* x;
+  int cin, h, w, kh, kw, stride, pad, ho, wo;
+  __device__ __forceinline__ float operator()(int64_t row, int col) const {
+    const int hw = ho * wo;
+    const int64_t b = row / hw;
+    const int pix = (int)(row - b * hw);
+    const int oy = pix / wo, ox = pix - (pix / wo) * wo;
+    const int kk = kh * kw;
+    const int ci = col / kk;
+    const int r = col - ci * kk;
+    const int dy = r / kw, dx = r - (r / kw) * kw;
+    const int iy = oy * stride + dy - pad, ix = ox * stride + dx - pad;
+    if (iy < 0 || iy >= h || ix < 0 || ix >= w) return 0.0f;
+    return __ldg(x + ((b * cin + ci) * (int64_t)h + iy) * w + ix);
+  }
+};
+
+// VT: compile-time register capacity for the sub-vector (0 = stream from memory)
+template <int VT, class Rows>
+__global__ void __launch_bounds__(256) encode_rows_kernel(Rows rows, int64_t n, const float* __restrict__ prep,
+                                                          int S, int C, int K, int V, uint8_t* __restrict__ codes,
+                                                          int code_bits, int64_t code_stride, int* near_tie) {
+  extern __shared__ float sh[];  // up to 2 prepared codebook records
+  const int cpt = (code_bits == 4) ? 2 : 1;  // codebooks per thread (nibble pairs share a byte)
+  const int c0 = blockIdx.y * cpt;
+  const int ncb = min(cpt, C - c0);
+  for (int i = threadIdx.x; i < ncb * S; i += blockDim.x) sh[i] = prep[(size_t)c0 * S + i];
+  __syncthreads();
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  const float tau_c = tau_coef(V);
+  uint32_t packed = 0;
+  for (int s = 0; s < ncb; ++s) {
+    const int c = c0 + s;
+    const float* cb = sh + s * S;
+    const float* norms = cb + K * V;
+    float best = FLT_MAX, second = FLT_MAX, asq = 0.0f;
+    int bi = 0;
+    if constexpr (VT > 0) {
+      float a[VT];
+#pragma unroll
+      for (int j = 0; j < VT; ++j) {
+        float x = (j < V) ? rows(row, c * V + j) : 0.0f;
+        asq = fmaf(x, x, asq);
+        a[j] = -2.0f * x;
+      }
+      for (int k = 0; k < K; ++k) {
+        float acc0 = norms[k], acc1 = 0.0f;
+        const float* pkv = cb + k * V;
+#pragma unroll
+        for (int j = 0; j < VT; ++j) {
+          if (j < V) {
+            if (j & 1) acc1 = fmaf(a[j], pkv[j], acc1);
+            else acc0 = fmaf(a[j], pkv[j], acc0);
+          }
+        }
+        const float d = acc0 + acc1;
+        second = fminf(second, fmaxf(best, d));
+        bi = (d < best) ? k : bi;
+        best = fminf(best, d);
+      }
+    } else {
+      for (int j = 0; j < V; ++j) {
+        float x = rows(row, c * V + j);
+        asq = fmaf(x, x, asq);
+      }
+      for (int k = 0; k < K; ++k) {
+        float acc0 = norms[k], acc1 = 0.0f;
+        const float* pkv = cb + k * V;
+        for (int j = 0; j < V; ++j) {
+          const float x = -2.0f * rows(row, c * V + j);
+          if (j & 1) acc1 = fmaf(x, pkv[j], acc1);
+          else acc0 = fmaf(x, pkv[j], acc0);
+        }
+        const float d = acc0 + acc1;
+        second = fminf(second, fmaxf(best, d));
+        bi = (d < best) ? k : bi;
+        best = fminf(best, d);
+      }
+    }
+    if (!(second - best > tau_c * (asq + norms[K]))) {
+      auto get_a = [&](int j) { return rows(row, c * V + j); };
+      bi = exact_argmin(get_a, cb, K, V);
+      if (near_tie) atomicAdd(near_tie, 1);
+    }
+    if (code_bits == 8) {
+      codes[row * code_stride + c] = (uint8_t)bi;
+    } else {
+      packed |= (uint32_t)bi << (4 * s);
+    }
+  }
+  if (code_bits == 4) codes[row * code_stride + c0 / 2] = (uint8_t)packed;
+}
+
+// ---------------------------------------------------------------- im2col
+
+__global__ void im2col_kernel(ConvRows rows, int64_t n, int d, float* __restrict__ cols) {
+  const int64_t total = n * d;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / d;
+    const int col = (int)(i - row * d);
+    cols[i] = rows(row, col);
+  }
+}
+
+// ------------------------------------------------------------ host launch
+
+static int launch_rows(const DenseRows* dense, const ConvRows* conv, int64_t n, const float* prep, int C,
+                       int K, int V, uint8_t* codes, int code_bits, int* near_tie, cudaStream_t stream) {
+  const int S = prep_stride(K, V);
+  const int cpt = code_bits == 4 ? 2 : 1;
+  const int64_t code_stride = code_bits == 4 ? (C + 1) / 2 : C;
+  dim3 grid((unsigned)((n + 255) / 256), (unsigned)((C + cpt - 1) / cpt));
+  const size_t smem = (size_t)cpt * S * sizeof(float);
+#define LUT_ROWS_LAUNCH(VT)                                                                            \
+  do {                                                                                                 \
+    if (dense) {                                                                                       \
+      auto kern = encode_rows_kernel<VT, DenseRows>;                                                   \
+      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      kern<<<grid, 256, smem, stream>>>(*dense, n, prep, S, C, K, V, codes, code_bits, code_stride, near_tie); \
+    } else {                                                                                           \
+      auto kern = encode_rows_kernel<VT, ConvRows>;                                                    \
+      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      kern<<<grid, 256, smem, stream>>>(*conv, n, prep, S, C, K, V, codes, code_bits, code_stride, near_tie); \
+    }                                                                                                  \
+  } while (0)
+  if (V <= 1) LUT_ROWS_LAUNCH(1);
+  else if (V <= 2) LUT_ROWS_LAUNCH(2);
+  else if (V <= 3) LUT_ROWS_LAUNCH(3);
+  else if (V <= 4) LUT_ROWS_LAUNCH(4);
+  else if (V <= 8) LUT_ROWS_LAUNCH(8);
+  else if (V <= 9) LUT_ROWS_LAUNCH(9);
+  else if (V <= 16) LUT_ROWS_LAUNCH(16);
+  else if (V <= 32) LUT_ROWS_LAUNCH(32);
+  else if (V <= 64) LUT_ROWS_LAUNCH(64);
+  else LUT_ROWS_LAUNCH(0);
+#undef LUT_ROWS_LAUNCH
+  LUT_CHECK_LAUNCH("encode_rows_kernel");
+  return LUT_OK;
+}
+
+template <int V>
+static int launch_tma(const float* a, int64_t n, int d, const float* prep, int C, int K, uint8_t* codes,
+                      int code_bits, int* near_tie, cudaStream_t stream, bool* used) {
+  *used = false;
+  const int S = prep_stride(K, V);
+  constexpr int NB = 32 / V;
+  const int book_bytes = NB * S * 4;
+  const int stage_bytes = ((kRPL * kBoxBytes + book_bytes) + 1023) & ~1023;
+  const size_t budget = max_smem_optin();
+  int stages = (int)((budget - 1024 - 256) / stage_bytes);
+  if (stages > 4) stages = 4;
+  if (stages < 2) return LUT_OK;  // does not fit: caller falls back
+  CUtensorMap tmap;
+  if (!make_tmap_2d_f32(&tmap, a, (uint64_t)d, (uint64_t)n, 32, kBoxRows, true)) return LUT_OK;
+
+  EncTmaParams p;
+  p.prep = prep;
+  p.S = S;
+  p.n = n;
+  p.C = C;
+  p.K = K;
+  p.code_bits = code_bits;
+  p.code_stride = code_bits == 4 ? (C + 1) / 2 : C;
+  p.codes = codes;
+  p.near_tie = near_tie;
+  p.stages = stages;
+  p.stage_bytes = stage_bytes;
+  p.ntiles = (n + kTileRows - 1) / kTileRows;
+  const int nsm = num_sms();
+  // group = flush granularity: 16 B of codes per row, shrunk until the grid fills the chip
+  // (powers of two >= NB, so a box never straddles groups; even for nibble pairs)
+  int G = code_bits == 8 ? 16 : 32;
+  const int gmin = (code_bits == 4 && NB < 2) ? 2 : NB;
+  while (G > gmin && p.ntiles * ((C + G - 1) / G) < 2LL * nsm) G /= 2;
+  p.G = G;
+  p.ngroups = (C + G - 1) / G;
+  const int64_t nunits = p.ntiles * p.ngroups;
+  const int grid = (int)(nunits < nsm ? nunits : nsm);
+  const size_t smem = (size_t)stages * stage_bytes + 2 * stages * sizeof(uint64_t) + 1024;
+  auto kern = encode_tma_kernel<V>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(encode_tma)");
+  kern<<<grid, kEncThreads, smem, stream>>>(tmap, p);
+  LUT_CHECK_LAUNCH("encode_tma_kernel");
+  *used = true;
+  return LUT_OK;
+}
+
+int encode_dense(const float* a, int64_t n, int d, const float* prep, int C, int K, int V, uint8_t* codes,
+                 int code_bits, int* near_tie, cudaStream_t stream, int force_generic) {
+  if (n == 0 || C == 0) return LUT_OK;
+  const bool aligned = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (reinterpret_cast<uintptr_t>(prep) & 15) == 0;
+  if (!force_generic && aligned && K <= 128 && n >= kTileRows / 2) {
+    bool used = false;
+    int st = LUT_OK;
+    switch (V) {
+      case 4: st = launch_tma<4>(a, n, d, prep, C, K, codes, code_bits, near_tie, stream, &used); break;
+      case 8: st = launch_tma<8>(a, n, d, prep, C, K, codes, code_bits, near_tie, stream, &used); break;
+      case 16: st = launch_tma<16>(a, n, d, prep, C, K, codes, code_bits, near_tie, stream, &used); break;
+      case 32: st = launch_tma<32>(a, n, d, prep, C, K, codes, code_bits, near_tie, stream, &used); break;
+      default: break;
+    }
+    if (st != LUT_OK) return st;
+    if (used) return LUT_OK;
+  }
+  DenseRows rows{a, d};
+  return launch_rows(&rows, nullptr, n, prep, C, K, V, codes, code_bits, near_tie, stream);
+}
+
+int encode_conv(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad,
+                const float* prep, int C, int K, int V, uint8_t* codes, int code_bits, int* near_tie,
+                cudaStream_t stream) {
+  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
+  const int64_t n = (int64_t)batch * ho * wo;
+  if (n == 0 || C == 0) return LUT_OK;
+  ConvRows rows{x, cin, h, w, kh, kw, stride, pad, ho, wo};
+  return launch_rows(nullptr, &rows, n, prep, C, K, V, codes, code_bits, near_tie, stream);
+}
+
+int im2col(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad, float* cols,
+           cudaStream_t stream) {
+  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
+  const int64_t n = (int64_t)batch * ho * wo;
+  const int d = cin * kh * kw;
+  if (n == 0 || d == 0) return LUT_OK;
+  ConvRows rows{x, cin, h, w, kh, kw, stride, pad, ho, wo};
+  const int64_t total = n * d;
+  const int blocks = (int)((total + 255) / 256 < 65535 * 8 ? (total + 255) / 256 : 65535 * 8);
+  im2col_kernel<<<blocks, 256, 0, stream>>>(rows, n, d, cols);
+  LUT_CHECK_LAUNCH("im2col_kernel");
+  return LUT_OK;
+}
+
+int prepare_books(const float* books, int C, int K, int V, float* prep, cudaStream_t stream) {
+  if (C == 0) return LUT_OK;
+  prepare_books_kernel<<<C, 128, 0, stream>>>(books, C, K, V, prep);
+  LUT_CHECK_LAUNCH("prepare_books_kernel");
+  return LUT_OK;
+}
+
+}  // namespace lutgpu

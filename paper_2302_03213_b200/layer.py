@@ -1,0 +1,227 @@
+"""Device-resident LUT layer — mirror of lutkit.softpq.LutLayer (softpq.py:82-172).
+
+Holds the codebooks (plus the prepared encode record), the f32 table and/or
+its int8 twin, the bias and an optional fused activation, all in HBM.  The
+layer is what `lut_layer_infer` consumes; a reference `LutLayer` (or any
+object with the same attributes) is converted once and cached."""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+
+import numpy as np
+import torch
+
+from . import _device as D
+from ._lib import LayerDesc, check, load
+from .errors import ConfigError, ShapeError
+from .kernels import ACTS, EncodeStats, prepare_books
+from .pq import PqConfig, build_table_device, validate_codebooks
+from .quant import LookupTableI8, dequantize, quantize_table
+
+F32 = np.float32
+PIPELINE_MIN_BYTES = 32 << 20   # numpy inputs above this stream through the native executor
+PIPELINE_CHUNK_BYTES = 256 << 20
+
+
+class LutLayer:
+    """One PQ-replaced linear layer on the GPU.
+
+    Arguments mirror the reference dataclass: cfg, books (C,K,V), weight (D,M)
+    or None, bias (M,) (empty = no bias add), qat (also build the int8 twin),
+    table / qtable (precomputed), trees (hash encoder).  Extensions: `act`
+    ("relu" / "gelu" fused into the epilogue) and `scale_mtile` (per-m-tile
+    int8 scales)."""
+
+    def __init__(self, cfg: PqConfig, books, weight=None, bias=None, qat: bool = False, table=None,
+                 qtable: LookupTableI8 | None = None, trees=None, act=None, scale_mtile: int = 0,
+                 device=None):
+        self.device = torch.device(device) if device is not None else D.require_cuda()
+        books = validate_codebooks(books)
+        c, k, v = D.shape_of(books)
+        if (k, v) != (cfg.k, cfg.v):
+            raise ShapeError(f"codebooks {(c, k, v)} inconsistent with config {cfg}")
+        if act not in ACTS:
+            raise ConfigError(f"unknown activation {act!r}")
+        self.cfg = cfg
+        self.qat = qat
+        self.trees = trees
+        self.act = act
+        self.scale_mtile = scale_mtile
+        self.books = D.to_device(books, F32, self.device)
+        self.books_prep = prepare_books(self.books)
+        self.weight = None
+        if weight is not None:
+            ws = D.shape_of(weight)
+            if len(ws) != 2:
+                raise ShapeError(f"weight must be 2-D, got shape {ws}")
+            if ws[0] != c * v:
+                raise ShapeError(f"weight rows {ws[0]} != C*V = {c * v}")
+            self.weight = D.to_device(weight, F32, self.device)
+        self.table = None if table is None else D.to_device(table, F32, self.device)
+        self.qtable = None
+        if qtable is not None:
+            self.qtable = LookupTableI8(q=D.to_device(qtable.q, np.int8, self.device),
+                                        scale=qtable.scales_tensor(self.device) if isinstance(qtable, LookupTableI8)
+                                        else torch.as_tensor(np.asarray(qtable.scale, F32).reshape(-1),
+                                                             device=self.device),
+                                        scale_mtile=getattr(qtable, "scale_mtile", 0))
+        if self.table is None and self.qtable is None:
+            self.rebuild()
+        m = self.m
+        if bias is None:
+            self.bias = torch.empty(0, dtype=torch.float32, device=self.device)
+        else:
+            self.bias = D.to_device(bias, F32, self.device).reshape(-1)
+            if self.bias.numel() not in (0, m):
+                raise ShapeError(f"bias has {self.bias.numel()} entries, expected {m}")
+        self._desc_cache = {}
+        self._pipelines = {}
+
+    # ------------------------------------------------------------ properties
+    @property
+    def c(self) -> int:
+        return self.books.shape[0]
+
+    @property
+    def k(self) -> int:
+        return self.cfg.k
+
+    @property
+    def v(self) -> int:
+        return self.cfg.v
+
+    @property
+    def d(self) -> int:
+        return self.c * self.cfg.v
+
+    @property
+    def m(self) -> int:
+        if self.table is not None:
+            return self.table.shape[2]
+        return self.qtable.q.shape[2]
+
+    @property
+    def has_qtable(self) -> bool:
+        return self.qtable is not None
+
+    # ----------------------------------------------------------- table build
+    def rebuild(self) -> None:
+        """Recompute table (and int8 twin under qat) from weight (softpq.py:125-132)."""
+        if self.weight is None:
+            if self.table is None and self.qtable is None:
+                raise ConfigError("layer has neither a weight matrix nor a table")
+            return
+        self.table = build_table_device(self.weight, self.books)
+        self.qtable = quantize_table(self.table, self.scale_mtile) if self.qat else None
+        self._desc_cache = {} if hasattr(self, "_desc_cache") else None
+
+    def forward_table(self):
+        """Table the training forward reads: dequantized under QAT (softpq.py:134-140)."""
+        if self.qat:
+            if self.qtable is None:
+                self.qtable = quantize_table(self.table, self.scale_mtile)
+            return dequantize(self.qtable)
+        return self.table
+
+    def quantize(self, scale_mtile: int | None = None) -> None:
+        """Build (or rebuild) the int8 twin from the f32 table."""
+        if scale_mtile is not None:
+            self.scale_mtile = scale_mtile
+        self.qtable = quantize_table(self.table, self.scale_mtile)
+        self._desc_cache = {}
+
+    # ---------------------------------------------------------------- ABI
+    def desc(self, integer: bool) -> LayerDesc:
+        key = bool(integer)
+        if key in self._desc_cache:
+            return self._desc_cache[key]
+        d = LayerDesc()
+        d.c, d.k, d.v, d.m = self.c, self.k, self.v, self.m
+        d.books_prep = D.ptr(self.books_prep)
+        d.table = D.ptr(self.table) if self.table is not None else None
+        if self.qtable is not None:
+            self._scales_dev = self.qtable.scales_tensor(self.device)
+            d.q = D.ptr(self.qtable.q)
+            d.scales = D.ptr(self._scales_dev)
+            d.scale_mtile = self.qtable.scale_mtile
+        d.bias = D.ptr(self.bias)
+        d.act = ACTS[self.act]
+        d.integer = 1 if integer else 0
+        self._desc_cache[key] = d
+        return d
+
+    def forward_device(self, a_dev: torch.Tensor, integer: bool, out: torch.Tensor | None = None,
+                       codes: torch.Tensor | None = None, near: torch.Tensor | None = None) -> torch.Tensor:
+        """(N, D) f32 CUDA -> (N, M) f32 CUDA through lut_layer_forward."""
+        n = a_dev.shape[0]
+        if out is None:
+            out = torch.empty((n, self.m), dtype=torch.float32, device=a_dev.device)
+        if codes is None:
+            codes = torch.empty((n, max(self.c, 1)), dtype=torch.uint8, device=a_dev.device)
+        check(load().lut_layer_forward(C.byref(self.desc(integer)), D.ptr(a_dev), n, D.ptr(out), D.ptr(codes),
+                                       D.ptr(near), D.stream_ptr()), "lut_layer_infer")
+        return out
+
+    def _pipeline(self, chunk_rows: int):
+        key = (self.device.index, chunk_rows)
+        p = self._pipelines.get(key)
+        if p is None:
+            handle = C.c_void_p()
+            check(load().lut_pipeline_create(self.device.index or 0, chunk_rows, self.d, self.m, self.c,
+                                             C.byref(handle)), "lut_pipeline_create")
+            p = handle
+            self._pipelines[key] = p
+            weakref.finalize(self, load().lut_pipeline_destroy, p)
+        return p
+
+    def infer(self, a, integer: bool, out=None):
+        kind = D.kind_of(a)
+        n = D.shape_of(a)[0]
+        if kind == D.NUMPY and n * self.d * 4 >= PIPELINE_MIN_BYTES:
+            a_h = np.ascontiguousarray(a, dtype=F32)
+            if out is None:
+                out = np.empty((n, self.m), dtype=F32)
+            elif out.shape != (n, self.m) or out.dtype != F32 or not out.flags.c_contiguous:
+                raise ShapeError(f"out must be a contiguous f32 array of shape {(n, self.m)}")
+            chunk = max(1, min(n, PIPELINE_CHUNK_BYTES // max(1, 4 * max(self.d, self.m))))
+            torch.cuda.current_stream().synchronize()
+            near = C.c_int32(0)
+            check(load().lut_pipeline_run(self._pipeline(chunk), C.byref(self.desc(integer)),
+                                          a_h.ctypes.data, n, out.ctypes.data, C.byref(near)), "lut_layer_infer")
+            EncodeStats.last_near_ties = near.value
+            return out
+        a_dev = D.to_device(a, F32, self.device)
+        res = self.forward_device(a_dev, integer)
+        if out is not None and kind == D.NUMPY:
+            out[...] = res.cpu().numpy()
+            return out
+        return D.from_device(res, kind)
+
+    def infer_hash(self, a, integer: bool):
+        raise ConfigError("hash encoder is not available on the GPU path in this build")
+
+
+_FOREIGN: dict[int, tuple] = {}
+
+
+def as_device_layer(layer) -> LutLayer:
+    """Our LutLayer as is; a reference-style layer converted once (cached
+    while its arrays are the same objects)."""
+    if isinstance(layer, LutLayer):
+        return layer
+    key = id(layer)
+    arrays = (layer.books, getattr(layer, "table", None), getattr(layer, "qtable", None), layer.bias)
+    hit = _FOREIGN.get(key)
+    if hit is not None and all(x is y for x, y in zip(hit[0], arrays)):
+        return hit[1]
+    qt = getattr(layer, "qtable", None)
+    if qt is not None and not isinstance(qt, LookupTableI8):
+        qt = LookupTableI8(q=np.asarray(qt.q), scale=F32(qt.scale))
+    cfg = layer.cfg if isinstance(getattr(layer, "cfg", None), PqConfig) else PqConfig(
+        v=int(layer.cfg.v), k=int(layer.cfg.k))
+    dl = LutLayer(cfg=cfg, books=layer.books, weight=None, bias=layer.bias, table=getattr(layer, "table", None),
+                  qtable=qt, trees=getattr(layer, "trees", None))
+    _FOREIGN[key] = (arrays, dl)
+    return dl

@@ -1,0 +1,157 @@
+"""CPU-only checks: the C-ABI library loads and exports every symbol the
+header declares; host-side validation raises the reference's exception
+classes before any device work; row-sharding host logic (gloo, 2 ranks)."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+F32 = np.float32
+
+
+def header_symbols():
+    with open(os.path.join(ROOT, "include", "lutgpu.h")) as f:
+        return sorted(set(re.findall(r"LUT_API\s+[\w\s\*]+?\b(lut_\w+)\s*\(", f.read())))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2302_03213_b200 import _lib
+
+    declared = header_symbols()
+    assert len(declared) >= 17
+    import ctypes
+
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(declared) == set(_lib.SIGNATURES), "ctypes signature table out of sync with the header"
+    h = _lib.load()
+    assert h.lut_version() == 100
+    assert h.lut_books_prep_bytes(128, 16, 32) == 128 * ((16 * 32 + 16 + 1 + 3) // 4 * 4) * 4
+
+
+def test_abi_rejects_bad_geometry_without_gpu():
+    """Shape/option errors are host-side: no device is touched."""
+    from paper_2302_03213_b200 import _lib
+
+    h = _lib.load()
+    assert h.lut_encode_f32(None, 10, 7, None, 2, 16, 4, None, 8, None, None) == 2  # d != C*V
+    assert h.lut_encode_f32(None, 10, 8, None, 2, 300, 4, None, 8, None, None) == 2  # K > 256
+    assert h.lut_encode_f32(None, 10, 8, None, 2, 32, 4, None, 4, None, None) == 2  # u4 with K > 16
+    assert b"4-bit" in h.lut_last_error()
+    assert h.lut_gather_f32(None, 8, 5, 2, 16, 4, None, None, 9, None, 0, None, None) == 2  # bad act
+    assert h.lut_gather_i8(None, 8, 5, 2, 16, 4, None, None, -1, None, 0, None, None, 0, None, None) == 2
+    assert h.lut_im2col_f32(None, 1, 1, 2, 2, 3, 3, 1, 0, None, None) == 2  # kernel does not fit
+    assert h.lut_pipeline_create(0, 0, 4, 4, 1, None) == 2
+
+
+def test_python_validation_matches_reference_exceptions():
+    import paper_2302_03213_b200 as L
+
+    with pytest.raises(L.ConfigError):
+        L.KernelPlan(group_size=259)
+    with pytest.raises(L.ConfigError):
+        L.KernelPlan(group_size=0)
+    L.KernelPlan(group_size=258)
+    assert L.MAX_GROUP == 258
+    with pytest.raises(L.ShapeError):
+        L.centroid_search_fast(np.zeros((1, 5), F32), np.zeros((2, 4, 3), F32))
+    with pytest.raises(L.ShapeError):
+        L.centroid_search_fast(np.zeros((5,), F32), np.zeros((2, 4, 3), F32))
+    with pytest.raises(L.ConfigError):
+        L.centroid_search_fast(np.zeros((1, 6), F32), np.zeros((2, 300, 3), F32))
+    with pytest.raises(L.ShapeError):
+        L.lut_gather_i32(np.zeros((2, 3), np.uint8), np.zeros((3, 4, 2), np.int16))
+    with pytest.raises(L.ShapeError):
+        L.lut_gather_i32(np.zeros((2, 2), np.uint8), np.zeros((3, 4, 2), np.int8))
+    with pytest.raises(L.ShapeError):
+        L.lut_gather_f32(np.zeros((2,), np.uint8), np.zeros((3, 4, 2), F32))
+    with pytest.raises(L.ConfigError):
+        L.PqConfig(v=0, k=4)
+    with pytest.raises(L.ConfigError):
+        L.PqConfig(v=2, k=257)
+    with pytest.raises(L.ShapeError):
+        L.build_table(np.zeros((5, 2), F32), np.zeros((2, 4, 3), F32))
+    with pytest.raises(L.ShapeError):
+        L.im2col(np.zeros((1, 1, 2, 2), F32), 3, 3)
+    with pytest.raises(L.ConfigError):
+        L.im2col(np.zeros((1, 1, 4, 4), F32), 2, 2, stride=0)
+    with pytest.raises(L.ShapeError):
+        L.LookupTableI8(q=np.zeros((2, 2), np.int8), scale=np.float32(1.0))
+    with pytest.raises(L.DataError):
+        L.LookupTableI8(q=np.zeros((1, 2, 2), np.int8), scale=np.float32(0.0))
+    with pytest.raises(L.DataError):
+        L.LookupTableI8(q=np.full((1, 2, 2), -128, np.int8), scale=np.float32(1.0))
+
+
+def test_compute_without_gpu_fails_loudly():
+    import torch
+
+    import paper_2302_03213_b200 as L
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(L.DeviceError):
+        L.centroid_search_fast(np.zeros((2, 6), F32), np.zeros((2, 4, 3), F32))
+
+
+def test_flop_counter():
+    import paper_2302_03213_b200 as L
+
+    c = L.flop_counter(100, 64, 128, 16, 8)
+    assert (c["encode"], c["lookup_aggregate"], c["dense"]) == (102400, 102400, 819200)
+    assert L.flop_counter(10**4, 768, 96, 16, 32)["encode"] == 122_880_000
+    with pytest.raises(L.ConfigError):
+        L.flop_counter(1, 10, 4, 4, 3)
+
+
+def test_shard_range_partitions_rows():
+    from paper_2302_03213_b200.dist import shard_range, shard_sizes
+
+    for n in (0, 1, 7, 1024, 2**20 + 3):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard_range(n, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            assert max(shard_sizes(n, world)) - min(shard_sizes(n, world)) <= 1
+
+
+def _gloo_worker(rank, world, port, n, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2302_03213_b200.dist import gather_rows, shard_range
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        full = torch.arange(n * 3, dtype=torch.float32).reshape(n, 3)
+        s, e = shard_range(n, rank, world)
+        # each rank "computes" its rows (an elementwise stand-in for the layer)
+        local = full[s:e] * 2 + 1
+        got = gather_rows(local, n)
+        q.put((rank, bool(torch.equal(got, full * 2 + 1))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [10, 7, 1])
+def test_gather_rows_gloo_world2(n):
+    import multiprocessing as mp
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    res = dict(q.get(timeout=10) for _ in range(2))
+    assert res == {0: True, 1: True}

@@ -1,0 +1,290 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden vectors and the pinned oracle, on the reference's own test cases."""
+
+import numpy as np
+import pytest
+
+import golden_cases as G
+from oracle import lut_oracle as O
+
+pytestmark = pytest.mark.gpu
+F32 = np.float32
+
+
+@pytest.fixture(scope="module")
+def L():
+    import paper_2302_03213_b200 as lg
+
+    return lg
+
+
+def test_encode25(L, golden):
+    for case in golden.cases("encode25"):
+        a, books = G.encode25_inputs(case)
+        plan = L.KernelPlan(n_block=case["n_block"], k_block=case["k_block"])
+        np.testing.assert_array_equal(L.centroid_search_fast(a, books, plan), golden.arrays[f"encode25_{case['seed']}"])
+
+
+def test_ties(L, golden):
+    a, books = G.ties_dup_inputs()
+    for plan in (L.KernelPlan(), L.KernelPlan(n_block=1, k_block=2), L.KernelPlan(k_block=3)):
+        got, ties = L.centroid_search_fast(a, books, plan, return_near_ties=True)
+        np.testing.assert_array_equal(got, golden.arrays["ties_dup"])
+        assert got[0, 0] == 2 and got[0, 1] == 0
+        assert ties == 8  # every (row, codebook) is an exact tie -> fp64 re-decision
+    books = np.array([[[0.0, 0.0], [2.0, 0.0]]], dtype=F32)
+    got = L.centroid_search_fast(np.array([[1.0, 5.0]], F32), books, L.KernelPlan(k_block=1))
+    np.testing.assert_array_equal(got, golden.arrays["ties_equi"])
+    books = np.array([[[0.0], [2.0], [2.0]]], dtype=F32)
+    got = np.concatenate([L.encode_hard(np.array([[1.0]], F32), books), L.encode_hard(np.array([[2.0]], F32), books)])
+    np.testing.assert_array_equal(got, golden.arrays["ties_lowest"])
+
+
+def test_crit1_equivalence(L, golden):
+    """Acceptance criterion 1 (tests/test_acceptance.py:53-103) on the GPU:
+    indices exact, f32 path bitwise, i32 bitwise, table/quant bitwise."""
+    meta = golden.cases("crit1")
+    for trial, a, books, b in G.crit1_inputs():
+        case = meta[trial]
+        codes = L.centroid_search_fast(a, books)
+        np.testing.assert_array_equal(codes, golden.arrays[f"crit1_codes_{trial}"], err_msg=str(trial))
+        table = L.build_table(b, books)
+        assert G.sha(table) == case["table_sha"], trial
+        layer = L.LutLayer(cfg=L.PqConfig(v=case["v"], k=case["k"]), books=books, weight=b,
+                           bias=np.zeros(case["m"], F32))
+        out = L.lut_layer_infer(a, layer, integer=False)
+        assert out.dtype == np.float32 and G.sha(out) == case["out_f32_sha"], trial
+        qt = L.quantize_table(table)
+        assert G.sha(qt.q) == case["q_sha"] and float(qt.scale) == case["scale"], trial
+        np.testing.assert_array_equal(L.lut_gather_i32(codes, qt.q), golden.arrays[f"crit1_i32_{trial}"])
+
+
+def test_gather_cases(L, golden):
+    for case in golden.cases("gather15"):
+        enc, q = G.gather15_inputs(case)
+        got = L.lut_gather_i32(enc, q, L.KernelPlan(group_size=case["group_size"]))
+        assert got.dtype == np.int32
+        np.testing.assert_array_equal(got, golden.arrays[f"gather15_{case['seed']}"])
+    enc, q = G.gather_c300_inputs()
+    np.testing.assert_array_equal(L.lut_gather_i32(enc, q), golden.arrays["gather_c300"])
+    got = L.lut_gather_i32(np.zeros((4, 258), np.uint8), np.full((258, 2, 3), 127, np.int8), L.KernelPlan(group_size=258))
+    assert (got == 258 * 127).all()
+    got = L.lut_gather_i32(np.zeros((1, 200), np.uint8), np.full((200, 1, 1), 127, np.int8))
+    assert got[0, 0] == 25400
+    qt = L.LookupTableI8(q=np.array([[[1, -2], [3, 4]]], np.int8), scale=np.float32(0.5))
+    np.testing.assert_array_equal(L.lut_gather_accumulate(np.array([[1]], np.uint8), qt), [[1.5, 2.0]])
+    enc, t = G.scale_once_inputs()
+    qt = L.quantize_table(t)
+    case = golden.cases("scale_once")
+    assert G.sha(qt.q) == case["q_sha"] and float(qt.scale) == case["scale"]
+    assert G.sha(L.lut_gather_accumulate(enc, qt)) == case["out_sha"]
+
+
+def test_bad_index_raises(L):
+    with pytest.raises(L.CorruptionError):
+        L.lut_gather_i32(np.array([[7]], np.uint8), np.zeros((1, 4, 2), np.int8))
+    with pytest.raises(L.CorruptionError):
+        L.lut_gather_f32(np.array([[4]], np.uint8), np.zeros((1, 4, 2), F32))
+    # device-side detection (codes already on the GPU, u8 dtype)
+    import torch
+
+    enc = torch.tensor([[0, 9]], dtype=torch.uint8, device="cuda")
+    with pytest.raises(L.CorruptionError):
+        L.lut_gather_f32(enc, torch.zeros((2, 4, 3), device="cuda"))
+    # and the flag is cleared: a valid call afterwards succeeds
+    ok = L.lut_gather_f32(torch.tensor([[0, 3]], dtype=torch.uint8, device="cuda"), torch.ones((2, 4, 3), device="cuda"))
+    assert ok.cpu().numpy().tolist() == [[2.0, 2.0, 2.0]]
+
+
+def test_integer_without_qtable_raises(L):
+    rng = O.make_rng(12345)
+    books = rng.standard_normal((4, 8, 3)).astype(F32)
+    w = rng.standard_normal((12, 5)).astype(F32)
+    layer = L.LutLayer(cfg=L.PqConfig(v=3, k=8), books=books, weight=w, bias=np.zeros(5, F32))
+    with pytest.raises(L.ConfigError):
+        L.lut_layer_infer(rng.standard_normal((3, 12)).astype(F32), layer, integer=True)
+
+
+def test_quant_kats(L, golden):
+    qk = golden.cases("quant")
+    for name in ("scale127", "endpoint", "endpoint_neg", "half_even"):
+        qt = L.quantize_table(np.asarray(qk[name]["vals"], F32).reshape(1, 1, -1))
+        assert qt.q.ravel().tolist() == qk[name]["q"] and float(qt.scale) == qk[name]["scale"], name
+    qt = L.quantize_table(np.zeros((2, 3, 4), F32))
+    assert float(qt.scale) == 1.0 and not qt.q.any()
+    for case in qk["random20"]:
+        rng = O.make_rng(case["seed"])
+        t = (rng.standard_normal((2, 4, 6)) * rng.uniform(0.01, 100)).astype(F32)
+        qt = L.quantize_table(t)
+        assert G.sha(qt.q) == case["q_sha"] and float(qt.scale) == case["scale"]
+    with pytest.raises(L.DataError):
+        L.quantize_table(np.array([[[np.nan, 1.0]]], F32))
+
+
+def test_pqamm(L, golden):
+    for case in golden.cases("pqamm"):
+        a, books, b = G.pqamm_inputs(case)
+        out = L.pq_amm(a, b, L.PqConfig(v=case["v"], k=case["k"]), books)
+        assert G.sha(out) == case["out_sha"], case["seed"]
+
+
+def test_im2col(L, golden):
+    for case in golden.cases("im2col"):
+        x, kh, kw, stride, pad = G.im2col_inputs(case)
+        cols = L.im2col(x, kh, kw, stride, pad)
+        assert list(cols.shape) == case["shape"] and G.sha(cols) == case["sha"]
+
+
+def test_cfg1(L, golden):
+    """BASELINE configs[0] end to end, bitwise against the reference."""
+    case = golden.cases("cfg1")
+    a, books, w = G.cfg1_inputs()
+    np.testing.assert_array_equal(L.centroid_search_fast(a, books), golden.arrays["cfg1_codes"])
+    layer = L.LutLayer(cfg=L.PqConfig(v=16, k=16), books=books, weight=w, bias=np.zeros(768, F32), qat=True)
+    assert G.sha(layer.table.cpu().numpy()) == case["table_sha"]
+    assert G.sha(layer.qtable.q.cpu().numpy()) == case["q_sha"]
+    assert float(layer.qtable.scale) == case["scale"]
+    assert G.sha(L.lut_layer_infer(a, layer, integer=False)) == case["out_f32_sha"]
+    assert G.sha(L.lut_layer_infer(a, layer, integer=True)) == case["out_i8_sha"]
+
+
+@pytest.mark.parametrize("k", [16, 64])
+def test_cfg5_subsample_codes(L, golden, k):
+    """configs[4] encode geometry (D=4096, V=32): the TMA kernel."""
+    a, books = G.cfg5s_inputs(k)
+    codes, ties = L.centroid_search_fast(a, books, return_near_ties=True)
+    np.testing.assert_array_equal(codes, golden.arrays[f"cfg5s_k{k}_codes"])
+    assert ties < codes.size * 1e-3
+
+
+def test_conv_fused(L, golden):
+    """configs[2] geometry: im2col fused into encode, NCHW fused into gather."""
+    case = golden.cases("conv")
+    x, books, wconv = G.conv_inputs()
+    layer = L.LutLayer(cfg=L.PqConfig(v=9, k=16), books=books, weight=wconv, bias=np.zeros(16, F32))
+    conv = L.LutConv(16, 3, 1, 1, layer)
+    y, _ = conv.forward(x)
+    assert y.shape == (2, 16, 8, 8)
+    assert G.sha(y) == case["nchw_sha"]
+    cols = L.im2col(x, 3, 3, 1, 1)
+    np.testing.assert_array_equal(L.centroid_search_fast(cols, books), golden.arrays["conv_codes"])
+
+
+# --------------------------------------------------------------- sweeps
+
+SHAPES = [  # (n, c, k, v, m) — TMA encode path needs v in {4,8,16,32} and n >= 256
+    (300, 8, 16, 32, 40), (1000, 24, 16, 16, 33), (777, 16, 64, 8, 17), (513, 12, 8, 4, 64),
+    (256, 3, 128, 32, 5), (1, 5, 16, 32, 7), (70, 7, 256, 3, 9), (129, 4, 1, 9, 12),
+    (200, 2, 16, 100, 6), (65, 9, 33, 64, 130), (600, 1, 16, 1, 1), (0, 4, 16, 4, 8),
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_sweep_against_oracle(L, shape):
+    n, c, k, v, m = shape
+    rng = O.make_rng(hash(shape) % (2**32))
+    a, books, b = O.random_instance(rng, n, c, k, v, m)
+    bias = rng.standard_normal(m).astype(F32)
+    want_codes = O.encode_hard(a, books)
+    codes = L.centroid_search_fast(a, books)
+    np.testing.assert_array_equal(codes, want_codes)
+    table = O.build_table(b, books)
+    assert L.build_table(b, books).tobytes() == table.tobytes()
+    layer = L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=books, weight=b, bias=bias, qat=True)
+    out = L.lut_layer_infer(a, layer, integer=False)
+    assert out.tobytes() == O.lut_layer_infer(a, books, table=table, bias=bias, integer=False).tobytes()
+    q, s = O.quantize_table(table)
+    out8 = L.lut_layer_infer(a, layer, integer=True)
+    assert out8.tobytes() == O.lut_layer_infer(a, books, q=q, scale=s, bias=bias).tobytes()
+
+
+def test_u4_codes_match_u8(L):
+    import torch
+
+    from paper_2302_03213_b200.kernels import encode_device, prepare_books
+
+    rng = O.make_rng(4)
+    for (n, c, v) in ((1000, 32, 32), (700, 15, 16), (90, 7, 3)):
+        a, books, _ = O.random_instance(rng, n, c, 16, v, 1)
+        a_d, b_d = torch.from_numpy(a).cuda(), torch.from_numpy(books).cuda()
+        prep = prepare_books(b_d)
+        u8 = encode_device(a_d, prep, c, 16, v, 8).cpu().numpy()
+        u4 = encode_device(a_d, prep, c, 16, v, 4).cpu().numpy()
+        lo, hi = u4 & 15, u4 >> 4
+        unpacked = np.stack([lo, hi], axis=2).reshape(n, -1)[:, :c]
+        np.testing.assert_array_equal(unpacked, u8)
+        np.testing.assert_array_equal(u8, O.encode_hard(a, books))
+
+
+def test_epilogues_extension(L):
+    """GELU / ReLU epilogues and per-m-tile int8 scales (BASELINE configs[1]
+    extensions; parity unpinned: oracle restatement, tolerance stated)."""
+    rng = O.make_rng(21)
+    n, c, k, v, m = 300, 24, 16, 32, 96
+    a, books, b = O.random_instance(rng, n, c, k, v, m)
+    b *= 0.02
+    bias = rng.standard_normal(m).astype(F32) * 0.1
+    table = O.build_table(b, books)
+    codes = O.encode_hard(a, books)
+    for act in ("relu", "gelu"):
+        layer = L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=books, weight=b, bias=bias, act=act)
+        got = L.lut_layer_infer(a, layer, integer=False)
+        pre = O.lut_matmul_ref(codes, table) + bias
+        want = np.maximum(pre, 0) if act == "relu" else O.gelu_erf(pre)
+        if act == "relu":
+            assert got.tobytes() == want.astype(F32).tobytes()
+        else:
+            np.testing.assert_allclose(got, want, rtol=1e-6, atol=1e-6)
+    layer = L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=books, weight=b, bias=bias, qat=True, scale_mtile=32)
+    q, scales = O.quantize_table_mtile(table, 32)
+    np.testing.assert_array_equal(layer.qtable.q.cpu().numpy(), q)
+    np.testing.assert_array_equal(layer.qtable.scale.cpu().numpy(), scales)
+    got = L.lut_layer_infer(a, layer, integer=True)
+    want = O.lut_gather_accumulate_mtile(codes, q, scales, 32) + bias
+    assert got.tobytes() == want.astype(F32).tobytes()
+
+
+def test_large_rows_properties(L):
+    """BASELINE configs[4] width at 64K rows (1 GiB of input): the pipelined
+    host executor equals the device path bitwise, sampled rows equal the
+    oracle, and outputs are row-permutation equivariant."""
+    import torch
+
+    n, d, m, v, k = 65536, 4096, 256, 32, 16
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn((n, d), generator=g, device="cuda")
+    rng = O.make_rng(55)
+    books = rng.standard_normal((d // v, k, v)).astype(F32)
+    w = (rng.standard_normal((d, m)) / np.sqrt(d)).astype(F32)
+    layer = L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=books, weight=w, qat=True)
+    out_dev = L.lut_layer_infer(a, layer, integer=False)
+    out_host = L.lut_layer_infer(a.cpu().numpy(), layer, integer=False)  # > 32 MiB -> native executor
+    assert out_dev.cpu().numpy().tobytes() == out_host.tobytes()
+    idx = np.sort(rng.choice(n, 192, replace=False))
+    a_s = a[torch.as_tensor(idx, device="cuda")].cpu().numpy()
+    table = O.build_table(w, books)
+    want = O.lut_layer_infer(a_s, books, table=table, integer=False)
+    assert out_host[idx].tobytes() == want.tobytes()
+    perm = torch.randperm(n, device="cuda", generator=g)
+    out_perm = L.lut_layer_infer(a[perm], layer, integer=False)
+    assert torch.equal(out_perm, out_dev[perm])
+    o8 = L.lut_layer_infer(a, layer, integer=True)
+    q, s = O.quantize_table(table)
+    want8 = O.lut_layer_infer(a_s, books, q=q, scale=s)
+    assert o8.cpu().numpy()[idx].tobytes() == want8.tobytes()
+
+
+def test_reference_style_layer_object(L):
+    """A duck-typed reference LutLayer (numpy arrays) is accepted as is."""
+    from types import SimpleNamespace
+
+    rng = O.make_rng(9)
+    a, books, b = O.random_instance(rng, 50, 6, 8, 3, 7)
+    table = O.build_table(b, books)
+    q, s = O.quantize_table(table)
+    ref_layer = SimpleNamespace(cfg=SimpleNamespace(v=3, k=8), books=books, table=table,
+                                qtable=SimpleNamespace(q=q, scale=s), bias=np.zeros(7, F32), trees=None)
+    got = L.lut_layer_infer(a, ref_layer)
+    assert got.tobytes() == O.lut_layer_infer(a, books, q=q, scale=s, bias=np.zeros(7, F32)).tobytes()
+    got = L.lut_layer_infer(a, ref_layer, integer=False)
+    assert got.tobytes() == O.lut_layer_infer(a, books, table=table, bias=np.zeros(7, F32), integer=False).tobytes()
