@@ -46,6 +46,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--gather", choices=["tensor", "cuda"], default="tensor",
+                   help="lookup engine: tcgen05 one-hot GEMM (int8 exact / f32 digit planes) or CUDA-core")
+    p.add_argument("--digits", type=int, default=4, help="f32 digit planes for the tensor engine")
     p.add_argument("--cpu-rows", type=int, default=0, help="CPU sample rows per core (0 = default)")
     return p.parse_args()
 
@@ -221,25 +224,37 @@ def main():
     g = torch.Generator(device=dev).manual_seed(1234)
     books = torch.randn((c, k, v), generator=g, device=dev)
     w = torch.randn((d, m), generator=g, device=dev) / math.sqrt(d)
-    layer = L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=books, weight=w, qat=integer)
+    layer = L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=books, weight=w, qat=integer, gather=args.gather,
+                       f32_digits=args.digits)
+    tensor = layer.uses_tensor_cores(integer)
+    config["gather"] = ("tcgen05 one-hot kind::i8" + ("" if integer else f", {args.digits} digit planes")) \
+        if tensor else "CUDA-core SMEM gather"
     n = args.rows
     ga = torch.Generator(device=dev).manual_seed(99 + rank)
     a = torch.randn((n, d), generator=ga, device=dev)
-    codes = torch.empty((n, c), dtype=torch.uint8, device=dev)
+    cstride = int(lib.lut_code_stride(c))
+    codes = torch.empty((n, cstride), dtype=torch.uint8, device=dev)
     out = torch.empty((n, m), dtype=torch.float32, device=dev)
     near = torch.zeros(1, dtype=torch.int32, device=dev)
     scales = layer.qtable.scales_tensor(dev) if integer else None
+    image = layer.onehot_image(integer) if tensor else None
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
+    desc = layer.desc(integer)
 
     def step(ev=None):
+        # encode -> lookup-aggregate, the two kernels of lut_layer_forward, timed apart
         if ev:
             ev[0].record(stream)
         check(lib.lut_encode_f32(a.data_ptr(), n, d, layer.books_prep.data_ptr(), c, k, v, codes.data_ptr(), 8,
-                                 near.data_ptr(), sp))
+                                 cstride, near.data_ptr(), sp))
         if ev:
             ev[1].record(stream)
-        if integer:
+        if tensor:
+            check(lib.lut_gather_onehot(codes.data_ptr(), cstride, n, c, k, m, 1 if integer else args.digits,
+                                        image.data_ptr(), scales.data_ptr() if integer else None, 0, None, 0,
+                                        out.data_ptr(), None, 0, sp))
+        elif integer:
             check(lib.lut_gather_i8(codes.data_ptr(), 8, n, c, k, m, layer.qtable.q.data_ptr(), scales.data_ptr(),
                                     0, None, 0, out.data_ptr(), None, 0, None, sp))
         else:

@@ -86,11 +86,13 @@ LUT_API int lut_prepare_books(const float* books, int32_t c, int32_t k, int32_t 
  * (row, codebook) whose best/second-best gap is inside the fp32 error bound is
  * re-decided in fp64 from literal differences and counted in
  * *near_tie_count (device int32, accumulated; may be NULL).
- * code_bits = 8 (u8) or 4 (packed nibbles, k <= 16).
+ * code_bits = 8 (u8) or 4 (packed nibbles, k <= 16); code_stride = bytes per
+ * code row (0 = dense: c for u8, ceil(c/2) for u4; the one-hot gather wants
+ * lut_code_stride(c)).
  */
 LUT_API int lut_encode_f32(const float* a, int64_t n, int32_t d, const void* books_prep,
                    int32_t c, int32_t k, int32_t v, uint8_t* codes, int32_t code_bits,
-                   int32_t* near_tie_count, lut_stream_t stream);
+                   int64_t code_stride, int32_t* near_tie_count, lut_stream_t stream);
 
 /*
  * Encode with im2col fused into the row loader: reads the NCHW batch directly;
@@ -151,6 +153,34 @@ LUT_API int lut_quantize_table(const float* table, int32_t c, int32_t k, int32_t
                        lut_stream_t stream);
 
 /*
+ * Tensor-core lookup-aggregate (Eq. 4: out = onehot(codes) . T as a
+ * tcgen05 kind::i8 GEMM with inner dim c*k; power-of-two k <= 128).
+ * The table is first laid out once per layer as a swizzled "B image":
+ *   digits == 1: from the int8 table q — the int32 sums are EXACT, so the
+ *                result is bitwise equal to lut_gather_i8 (kernels.py:105-135);
+ *   digits == 2 or 4: from an f32 table, as balanced int8 digit planes of
+ *                s_m * t (per-column scale s_m, |t| <= 2^(8*digits-2)); sums are
+ *                exact integers rounded once to f32 (|error| <= c * s_m / 2;
+ *                4 digits: c * max|T[:,:,m]| * 2^-31), within the fp32 contract.
+ * lut_onehot_image_bytes() returns 0 when the shape is not supported.
+ * codes rows must be 16-byte aligned: code_stride % 16 == 0 (use the padded
+ * stride lut_code_stride()); codes are not range-checked on this path
+ * (use it on codes produced by lut_encode_f32).
+ */
+LUT_API size_t lut_onehot_image_bytes(int32_t c, int32_t k, int32_t m, int32_t digits);
+LUT_API int lut_onehot_prepare_i8(const int8_t* q, int32_t c, int32_t k, int32_t m, void* image,
+                                  lut_stream_t stream);
+LUT_API int lut_onehot_prepare_f32(const float* table, int32_t c, int32_t k, int32_t m, int32_t digits,
+                                   void* image, int32_t* err_flag, lut_stream_t stream);
+LUT_API int lut_gather_onehot(const uint8_t* codes, int64_t code_stride, int64_t n, int32_t c, int32_t k,
+                              int32_t m, int32_t digits, const void* image, const float* scales,
+                              int32_t scale_mtile, const float* bias, int32_t act, float* out,
+                              int32_t* out_i32, int64_t out_hw, lut_stream_t stream);
+
+/* Padded u8 code row stride (bytes) used by the layer path: round_up(c, 16). */
+LUT_API int64_t lut_code_stride(int32_t c);
+
+/*
  * Synchronize `stream`, read and clear the device error flag; returns the
  * status it held (LUT_OK, LUT_ERR_DATA or LUT_ERR_CORRUPTION) or LUT_ERR_CUDA.
  */
@@ -169,12 +199,15 @@ typedef struct lut_layer_desc {
   const float* bias;       /* (m) or NULL */
   int32_t act;             /* lut_act */
   int32_t integer;         /* 1 -> int8 path (needs q), 0 -> f32 path (needs table) */
+  const void* onehot_image; /* optional tensor-core B image for the selected path, or NULL */
+  int32_t onehot_digits;   /* 1 for the int8 path; 2 or 4 for the f32 path */
 } lut_layer_desc;
 
 /*
  * Full layer: encode -> lookup-aggregate -> bias/act.  Replaces
- * lut_layer_infer (kernels.py:143-178) with encoder="dist".
- * codes_scratch: n * c bytes (device).
+ * lut_layer_infer (kernels.py:143-178) with encoder="dist".  With an
+ * onehot_image the lookup runs on the tensor cores, else on the CUDA cores.
+ * codes_scratch: n * lut_code_stride(c) bytes (device, 16-byte aligned).
  */
 LUT_API int lut_layer_forward(const lut_layer_desc* layer, const float* a, int64_t n, float* out,
                       uint8_t* codes_scratch, int32_t* near_tie_count, lut_stream_t stream);

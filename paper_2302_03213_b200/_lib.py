@@ -30,6 +30,8 @@ class LayerDesc(C.Structure):
         ("bias", C.c_void_p),
         ("act", C.c_int32),
         ("integer", C.c_int32),
+        ("onehot_image", C.c_void_p),
+        ("onehot_digits", C.c_int32),
     ]
 
 
@@ -42,7 +44,7 @@ SIGNATURES = {
     "lut_last_error": (C.c_char_p, []),
     "lut_books_prep_bytes": (C.c_size_t, [I32, I32, I32]),
     "lut_prepare_books": (C.c_int, [P, I32, I32, I32, P, P]),
-    "lut_encode_f32": (C.c_int, [P, I64, I32, P, I32, I32, I32, P, I32, P, P]),
+    "lut_encode_f32": (C.c_int, [P, I64, I32, P, I32, I32, I32, P, I32, I64, P, P]),
     "lut_encode_conv_f32": (C.c_int, [P, I32, I32, I32, I32, I32, I32, I32, I32, P, I32, I32, I32, P, I32, P, P]),
     "lut_im2col_f32": (C.c_int, [P, I32, I32, I32, I32, I32, I32, I32, I32, P, P]),
     "lut_gather_f32": (C.c_int, [P, I32, I64, I32, I32, I32, P, P, I32, P, I64, P, P]),
@@ -51,6 +53,11 @@ SIGNATURES = {
     "lut_quantize_scratch_bytes": (C.c_size_t, [I32, I32, I32, I32]),
     "lut_quantize_table": (C.c_int, [P, I32, I32, I32, I32, P, P, P, P, P]),
     "lut_read_status": (C.c_int, [P, P]),
+    "lut_onehot_image_bytes": (C.c_size_t, [I32, I32, I32, I32]),
+    "lut_onehot_prepare_i8": (C.c_int, [P, I32, I32, I32, P, P]),
+    "lut_onehot_prepare_f32": (C.c_int, [P, I32, I32, I32, I32, P, P, P]),
+    "lut_gather_onehot": (C.c_int, [P, I64, I64, I32, I32, I32, I32, P, P, I32, P, I32, P, P, I64, P]),
+    "lut_code_stride": (I64, [I32]),
     "lut_layer_forward": (C.c_int, [C.POINTER(LayerDesc), P, I64, P, P, P, P]),
     "lut_pipeline_create": (C.c_int, [I32, I64, I32, I32, I32, C.POINTER(C.c_void_p)]),
     "lut_pipeline_run": (C.c_int, [P, C.POINTER(LayerDesc), P, I64, P, c_int32_p]),

@@ -15,7 +15,14 @@ namespace lutgpu {
 // kernels (encode.cu / gather.cu / table.cu)
 int prepare_books(const float* books, int C, int K, int V, float* prep, cudaStream_t stream);
 int encode_dense(const float* a, int64_t n, int d, const float* prep, int C, int K, int V, uint8_t* codes,
-                 int code_bits, int* near_tie, cudaStream_t stream, int force_generic);
+                 int code_bits, int64_t code_stride, int* near_tie, cudaStream_t stream, int force_generic);
+int onehot_supported(int C, int K, int M, int digits);
+size_t onehot_image_bytes(int C, int K, int M, int digits);
+int onehot_prepare_i8(const int8_t* q, int C, int K, int M, void* image, cudaStream_t stream);
+int onehot_prepare_f32(const float* t, int C, int K, int M, int digits, void* image, int* err, cudaStream_t stream);
+int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, int K, int M, int digits,
+                  const void* image, const float* scales, int scale_mtile, const float* bias, int act, float* out,
+                  int32_t* out_i32, int64_t out_hw, cudaStream_t stream);
 int encode_conv(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad,
                 const float* prep, int C, int K, int V, uint8_t* codes, int code_bits, int* near_tie,
                 cudaStream_t stream);
@@ -27,6 +34,12 @@ int gather_f32(const uint8_t* codes, int code_bits, int64_t n, int C, int K, int
 int gather_i8(const uint8_t* codes, int code_bits, int64_t n, int C, int K, int M, const int8_t* q,
               const float* scales, int scale_mtile, const float* bias, int act, float* out, int32_t* out_i32,
               int64_t out_hw, int* err, cudaStream_t stream, int force_generic);
+int gather_f32_strided(const uint8_t* codes, int code_bits, int64_t code_stride, int64_t n, int C, int K, int M,
+                       const float* table, const float* bias, int act, float* out, int64_t out_hw, int* err,
+                       cudaStream_t stream, int force_generic);
+int gather_i8_strided(const uint8_t* codes, int code_bits, int64_t code_stride, int64_t n, int C, int K, int M,
+                      const int8_t* q, const float* scales, int scale_mtile, const float* bias, int act, float* out,
+                      int32_t* out_i32, int64_t out_hw, int* err, cudaStream_t stream, int force_generic);
 int build_table(const float* b, int M, const float* books, int C, int K, int V, float* table,
                 cudaStream_t stream);
 size_t quantize_scratch_bytes(int C, int K, int M, int mtile);
@@ -164,14 +177,18 @@ int lut_prepare_books(const float* books, int32_t c, int32_t k, int32_t v, void*
 }
 
 int lut_encode_f32(const float* a, int64_t n, int32_t d, const void* books_prep, int32_t c, int32_t k, int32_t v,
-                   uint8_t* codes, int32_t code_bits, int32_t* near_tie_count, lut_stream_t stream) {
+                   uint8_t* codes, int32_t code_bits, int64_t code_stride, int32_t* near_tie_count,
+                   lut_stream_t stream) {
   LUT_TRY(check_geometry(c, k, v));
   LUT_TRY(check_codes(code_bits, k));
   if (n < 0) return fail(LUT_ERR_CONFIG, "row count must be >= 0");
   if ((int64_t)c * v != d) return fail(LUT_ERR_CONFIG, "input cols != C*V");
   if (n > 0 && c > 0 && (!a || !books_prep || !codes)) return fail(LUT_ERR_CONFIG, "null pointer");
-  return encode_dense(a, n, d, static_cast<const float*>(books_prep), c, k, v, codes, code_bits, near_tie_count,
-                      (cudaStream_t)stream, force_generic_env());
+  const int64_t dense = code_bits == 4 ? (c + 1) / 2 : c;
+  if (code_stride != 0 && code_stride < dense) return fail(LUT_ERR_CONFIG, "code_stride smaller than a code row");
+  const int64_t stride = code_stride ? code_stride : dense;
+  return encode_dense(a, n, d, static_cast<const float*>(books_prep), c, k, v, codes, code_bits, stride,
+                      near_tie_count, (cudaStream_t)stream, force_generic_env());
 }
 
 static int conv_dims(int32_t batch, int32_t cin, int32_t h, int32_t w, int32_t kh, int32_t kw, int32_t stride,
@@ -253,6 +270,42 @@ int lut_quantize_table(const float* table, int32_t c, int32_t k, int32_t m, int3
   return quantize_table(table, c, k, m, scale_mtile, q, scales, scratch, err_flag, (cudaStream_t)stream);
 }
 
+size_t lut_onehot_image_bytes(int32_t c, int32_t k, int32_t m, int32_t digits) {
+  if (c < 1 || k < 1 || m < 1) return 0;
+  if (!onehot_supported(c, k, m, digits)) return 0;
+  return onehot_image_bytes(c, k, m, digits);
+}
+
+int lut_onehot_prepare_i8(const int8_t* q, int32_t c, int32_t k, int32_t m, void* image, lut_stream_t stream) {
+  if (!lut_onehot_image_bytes(c, k, m, 1)) return fail(LUT_ERR_CONFIG, "shape not supported by the one-hot gather");
+  if (!q || !image) return fail(LUT_ERR_CONFIG, "null pointer");
+  return onehot_prepare_i8(q, c, k, m, image, (cudaStream_t)stream);
+}
+
+int lut_onehot_prepare_f32(const float* table, int32_t c, int32_t k, int32_t m, int32_t digits, void* image,
+                           int32_t* err_flag, lut_stream_t stream) {
+  if (digits < 2 || !lut_onehot_image_bytes(c, k, m, digits))
+    return fail(LUT_ERR_CONFIG, "shape/digits not supported by the one-hot gather");
+  if (!table || !image) return fail(LUT_ERR_CONFIG, "null pointer");
+  return onehot_prepare_f32(table, c, k, m, digits, image, err_flag, (cudaStream_t)stream);
+}
+
+int lut_gather_onehot(const uint8_t* codes, int64_t code_stride, int64_t n, int32_t c, int32_t k, int32_t m,
+                      int32_t digits, const void* image, const float* scales, int32_t scale_mtile, const float* bias,
+                      int32_t act, float* out, int32_t* out_i32, int64_t out_hw, lut_stream_t stream) {
+  LUT_TRY(check_act(act));
+  if (n < 0 || m < 0 || out_hw < 0 || scale_mtile < 0) return fail(LUT_ERR_CONFIG, "negative size");
+  if (out_hw > 0 && n % out_hw != 0) return fail(LUT_ERR_CONFIG, "rows not a multiple of out_hw");
+  if (!lut_onehot_image_bytes(c, k, m, digits)) return fail(LUT_ERR_CONFIG, "shape not supported by the one-hot gather");
+  if (n > 0 && (!codes || !image || (!out && !out_i32))) return fail(LUT_ERR_CONFIG, "null pointer");
+  if (digits == 1 && out && !scales) return fail(LUT_ERR_CONFIG, "null scales");
+  if (digits > 1 && out_i32) return fail(LUT_ERR_CONFIG, "int32 output only exists for digits == 1");
+  return onehot_gather(codes, code_stride, n, c, k, m, digits, image, scales, scale_mtile, bias, act, out, out_i32,
+                       out_hw, (cudaStream_t)stream);
+}
+
+int64_t lut_code_stride(int32_t c) { return c <= 0 ? 16 : ((int64_t)c + 15) / 16 * 16; }
+
 int lut_read_status(int32_t* err_flag, lut_stream_t stream) {
   cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
@@ -294,13 +347,19 @@ int lut_layer_forward(const lut_layer_desc* L, const float* a, int64_t n, float*
   if (!out || (L->c > 0 && (!a || !codes_scratch))) return fail(LUT_ERR_CONFIG, "null pointer");
   cudaStream_t s = (cudaStream_t)stream;
   const int d = L->c * L->v;
-  LUT_TRY(encode_dense(a, n, d, static_cast<const float*>(L->books_prep), L->c, L->k, L->v, codes_scratch, 8,
+  const int64_t stride = lut_code_stride(L->c);
+  LUT_TRY(encode_dense(a, n, d, static_cast<const float*>(L->books_prep), L->c, L->k, L->v, codes_scratch, 8, stride,
                        near_tie_count, s, force_generic_env()));
+  if (L->onehot_image) {
+    const int digits = L->integer ? 1 : L->onehot_digits;
+    return onehot_gather(codes_scratch, stride, n, L->c, L->k, L->m, digits, L->onehot_image, L->scales,
+                         L->scale_mtile, L->bias, L->act, out, nullptr, 0, s);
+  }
   if (L->integer)
-    return gather_i8(codes_scratch, 8, n, L->c, L->k, L->m, L->q, L->scales, L->scale_mtile, L->bias, L->act, out,
-                     nullptr, 0, nullptr, s, force_generic_env());
-  return gather_f32(codes_scratch, 8, n, L->c, L->k, L->m, L->table, L->bias, L->act, out, 0, nullptr, s,
-                    force_generic_env());
+    return gather_i8_strided(codes_scratch, 8, stride, n, L->c, L->k, L->m, L->q, L->scales, L->scale_mtile, L->bias,
+                             L->act, out, nullptr, 0, nullptr, s, force_generic_env());
+  return gather_f32_strided(codes_scratch, 8, stride, n, L->c, L->k, L->m, L->table, L->bias, L->act, out, 0, nullptr,
+                            s, force_generic_env());
 }
 
 // --------------------------------------------------------- host executor
@@ -357,7 +416,7 @@ int lut_pipeline_create(int32_t device, int64_t chunk_rows, int32_t d, int32_t m
   for (int i = 0; i < 2 && ok; ++i) {
     ok &= cudaMalloc(&p->dA[i], (size_t)chunk_rows * (d > 0 ? d : 1) * sizeof(float)) == cudaSuccess;
     ok &= cudaMalloc(&p->dOut[i], (size_t)chunk_rows * (m > 0 ? m : 1) * sizeof(float)) == cudaSuccess;
-    ok &= cudaMalloc(&p->dCodes[i], (size_t)chunk_rows * (c > 0 ? c : 1)) == cudaSuccess;
+    ok &= cudaMalloc(&p->dCodes[i], (size_t)chunk_rows * lut_code_stride(c)) == cudaSuccess;
     ok &= cudaEventCreateWithFlags(&p->ev_in[i], cudaEventDisableTiming) == cudaSuccess;
     ok &= cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming) == cudaSuccess;
     ok &= cudaEventCreateWithFlags(&p->ev_out[i], cudaEventDisableTiming) == cudaSuccess;

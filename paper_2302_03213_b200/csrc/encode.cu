@@ -452,10 +452,10 @@ __global__ void im2col_kernel(ConvRows rows, int64_t n, int d, float* __restrict
 // ------------------------------------------------------------ host launch
 
 static int launch_rows(const DenseRows* dense, const ConvRows* conv, int64_t n, const float* prep, int C,
-                       int K, int V, uint8_t* codes, int code_bits, int* near_tie, cudaStream_t stream) {
+                       int K, int V, uint8_t* codes, int code_bits, int64_t code_stride, int* near_tie,
+                       cudaStream_t stream) {
   const int S = prep_stride(K, V);
   const int cpt = code_bits == 4 ? 2 : 1;
-  const int64_t code_stride = code_bits == 4 ? (C + 1) / 2 : C;
   dim3 grid((unsigned)((n + 255) / 256), (unsigned)((C + cpt - 1) / cpt));
   const size_t smem = (size_t)cpt * S * sizeof(float);
 #define LUT_ROWS_LAUNCH(VT)                                                                            \
@@ -487,7 +487,7 @@ static int launch_rows(const DenseRows* dense, const ConvRows* conv, int64_t n, 
 
 template <int V>
 static int launch_tma(const float* a, int64_t n, int d, const float* prep, int C, int K, uint8_t* codes,
-                      int code_bits, int* near_tie, cudaStream_t stream, bool* used) {
+                      int code_bits, int64_t code_stride, int* near_tie, cudaStream_t stream, bool* used) {
   *used = false;
   const int S = prep_stride(K, V);
   constexpr int NB = 32 / V;
@@ -507,7 +507,7 @@ static int launch_tma(const float* a, int64_t n, int d, const float* prep, int C
   p.C = C;
   p.K = K;
   p.code_bits = code_bits;
-  p.code_stride = code_bits == 4 ? (C + 1) / 2 : C;
+  p.code_stride = code_stride;
   p.codes = codes;
   p.near_tie = near_tie;
   p.stages = stages;
@@ -534,24 +534,24 @@ static int launch_tma(const float* a, int64_t n, int d, const float* prep, int C
 }
 
 int encode_dense(const float* a, int64_t n, int d, const float* prep, int C, int K, int V, uint8_t* codes,
-                 int code_bits, int* near_tie, cudaStream_t stream, int force_generic) {
+                 int code_bits, int64_t code_stride, int* near_tie, cudaStream_t stream, int force_generic) {
   if (n == 0 || C == 0) return LUT_OK;
   const bool aligned = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (reinterpret_cast<uintptr_t>(prep) & 15) == 0;
   if (!force_generic && aligned && K <= 128 && n >= kTileRows / 2) {
     bool used = false;
     int st = LUT_OK;
     switch (V) {
-      case 4: st = launch_tma<4>(a, n, d, prep, C, K, codes, code_bits, near_tie, stream, &used); break;
-      case 8: st = launch_tma<8>(a, n, d, prep, C, K, codes, code_bits, near_tie, stream, &used); break;
-      case 16: st = launch_tma<16>(a, n, d, prep, C, K, codes, code_bits, near_tie, stream, &used); break;
-      case 32: st = launch_tma<32>(a, n, d, prep, C, K, codes, code_bits, near_tie, stream, &used); break;
+      case 4: st = launch_tma<4>(a, n, d, prep, C, K, codes, code_bits, code_stride, near_tie, stream, &used); break;
+      case 8: st = launch_tma<8>(a, n, d, prep, C, K, codes, code_bits, code_stride, near_tie, stream, &used); break;
+      case 16: st = launch_tma<16>(a, n, d, prep, C, K, codes, code_bits, code_stride, near_tie, stream, &used); break;
+      case 32: st = launch_tma<32>(a, n, d, prep, C, K, codes, code_bits, code_stride, near_tie, stream, &used); break;
       default: break;
     }
     if (st != LUT_OK) return st;
     if (used) return LUT_OK;
   }
   DenseRows rows{a, d};
-  return launch_rows(&rows, nullptr, n, prep, C, K, V, codes, code_bits, near_tie, stream);
+  return launch_rows(&rows, nullptr, n, prep, C, K, V, codes, code_bits, code_stride, near_tie, stream);
 }
 
 int encode_conv(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad,
@@ -561,7 +561,8 @@ int encode_conv(const float* x, int batch, int cin, int h, int w, int kh, int kw
   const int64_t n = (int64_t)batch * ho * wo;
   if (n == 0 || C == 0) return LUT_OK;
   ConvRows rows{x, cin, h, w, kh, kw, stride, pad, ho, wo};
-  return launch_rows(nullptr, &rows, n, prep, C, K, V, codes, code_bits, near_tie, stream);
+  const int64_t code_stride = code_bits == 4 ? (C + 1) / 2 : C;
+  return launch_rows(nullptr, &rows, n, prep, C, K, V, codes, code_bits, code_stride, near_tie, stream);
 }
 
 int im2col(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad, float* cols,

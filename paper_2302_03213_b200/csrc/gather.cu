@@ -237,6 +237,10 @@ __global__ void __launch_bounds__(kGatherThreads)
   const int64_t rb_per = (nrb + cpm - 1) / cpm;
   const int64_t rb0 = split * rb_per, rb1 = min(nrb, rb0 + rb_per);
   const int mt_step = gridDim.x >= (unsigned)nmt ? nmt : gridDim.x;
+  const bool words = (g.code_stride & 3) == 0 && (reinterpret_cast<uintptr_t>(g.codes) & 3) == 0;
+  const int span = g.code_bits == 8 ? 4 : 8;
+  uint32_t cw[RPT];
+  int have = 0;
 
   for (int mt = first_mt; mt < nmt; mt += mt_step) {
     const int m0 = mt * MT;
@@ -266,10 +270,26 @@ __global__ void __launch_bounds__(kGatherThreads)
 #pragma unroll
           for (int i = 0; i < 4; ++i) lo[r][i] = hi[r][i] = 0u;
         for (int c = c0; c < c1; ++c) {
+          if (words && (c & (span - 1)) == 0 && c + span <= c1) {
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+              const int64_t rr = rows[r] < g.n ? rows[r] : g.n - 1;
+              cw[r] = __ldg(reinterpret_cast<const uint32_t*>(g.codes + rr * g.code_stride +
+                                                             (g.code_bits == 8 ? c : (c >> 1))));
+            }
+            have = span;
+          }
 #pragma unroll
           for (int r = 0; r < RPT; ++r) {
-            const int64_t rr = rows[r] < g.n ? rows[r] : g.n - 1;
-            const int code = checked(g, read_code(g, rr, c));
+            int code;
+            if (have > 0) {
+              code = g.code_bits == 8 ? (int)(cw[r] & 255u) : (int)(cw[r] & 15u);
+              cw[r] = g.code_bits == 8 ? (cw[r] >> 8) : (cw[r] >> 4);
+            } else {
+              const int64_t rr = rows[r] < g.n ? rows[r] : g.n - 1;
+              code = read_code(g, rr, c);
+            }
+            code = checked(g, code);
             const uint4 t = qsm4[((c * g.K + code) * MT >> 4) + ql];
             lo[r][0] += t.x & 0x00FF00FFu;
             hi[r][0] += (t.x >> 8) & 0x00FF00FFu;
@@ -280,6 +300,7 @@ __global__ void __launch_bounds__(kGatherThreads)
             lo[r][3] += t.w & 0x00FF00FFu;
             hi[r][3] += (t.w >> 8) & 0x00FF00FFu;
           }
+          if (have > 0) --have;
         }
         const int bias128 = 128 * (c1 - c0);
 #pragma unroll
@@ -355,11 +376,12 @@ static int launch_tiled(void (*kern)(GatherArgs, const T*), int nmt, size_t smem
   return LUT_OK;
 }
 
-int gather_f32(const uint8_t* codes, int code_bits, int64_t n, int C, int K, int M, const float* table,
-               const float* bias, int act, float* out, int64_t out_hw, int* err, cudaStream_t stream,
-               int force_generic) {
+int gather_f32_strided(const uint8_t* codes, int code_bits, int64_t code_stride, int64_t n, int C, int K, int M,
+                       const float* table, const float* bias, int act, float* out, int64_t out_hw, int* err,
+                       cudaStream_t stream, int force_generic) {
   if (n == 0 || M == 0) return LUT_OK;
   GatherArgs g = make_args(codes, code_bits, n, C, K, M, bias, act, out, nullptr, out_hw, err);
+  g.code_stride = code_stride;
   const size_t budget = 200 * 1024;
   const size_t per_col = (size_t)C * K * sizeof(float);
   int MT = 0;
@@ -391,11 +413,12 @@ int gather_f32(const uint8_t* codes, int code_bits, int64_t n, int C, int K, int
   return LUT_OK;
 }
 
-int gather_i8(const uint8_t* codes, int code_bits, int64_t n, int C, int K, int M, const int8_t* q,
-              const float* scales, int scale_mtile, const float* bias, int act, float* out, int32_t* out_i32,
-              int64_t out_hw, int* err, cudaStream_t stream, int force_generic) {
+int gather_i8_strided(const uint8_t* codes, int code_bits, int64_t code_stride, int64_t n, int C, int K, int M,
+                      const int8_t* q, const float* scales, int scale_mtile, const float* bias, int act, float* out,
+                      int32_t* out_i32, int64_t out_hw, int* err, cudaStream_t stream, int force_generic) {
   if (n == 0 || M == 0) return LUT_OK;
   GatherArgs g = make_args(codes, code_bits, n, C, K, M, bias, act, out, out_i32, out_hw, err);
+  g.code_stride = code_stride;
   g.scales = scales;
   g.scale_mtile = scale_mtile;
   const size_t budget = 200 * 1024;
@@ -426,6 +449,24 @@ int gather_i8(const uint8_t* codes, int code_bits, int64_t n, int C, int K, int 
   if (st != LUT_OK) return st;
   LUT_CHECK_LAUNCH("gather_i8_tiled");
   return LUT_OK;
+}
+
+}  // namespace lutgpu
+
+namespace lutgpu {
+
+int gather_f32(const uint8_t* codes, int code_bits, int64_t n, int C, int K, int M, const float* table,
+               const float* bias, int act, float* out, int64_t out_hw, int* err, cudaStream_t stream,
+               int force_generic) {
+  return gather_f32_strided(codes, code_bits, code_bits == 4 ? (C + 1) / 2 : C, n, C, K, M, table, bias, act, out,
+                            out_hw, err, stream, force_generic);
+}
+
+int gather_i8(const uint8_t* codes, int code_bits, int64_t n, int C, int K, int M, const int8_t* q,
+              const float* scales, int scale_mtile, const float* bias, int act, float* out, int32_t* out_i32,
+              int64_t out_hw, int* err, cudaStream_t stream, int force_generic) {
+  return gather_i8_strided(codes, code_bits, code_bits == 4 ? (C + 1) / 2 : C, n, C, K, M, q, scales, scale_mtile,
+                           bias, act, out, out_i32, out_hw, err, stream, force_generic);
 }
 
 }  // namespace lutgpu

@@ -123,7 +123,7 @@ def encode_device(a_dev: torch.Tensor, prep: torch.Tensor, c: int, k: int, v: in
     n = a_dev.shape[0]
     width = c if code_bits == 8 else (c + 1) // 2
     codes = torch.empty((n, width), dtype=torch.uint8, device=a_dev.device)
-    check(lib.lut_encode_f32(D.ptr(a_dev), n, c * v, D.ptr(prep), c, k, v, D.ptr(codes), code_bits,
+    check(lib.lut_encode_f32(D.ptr(a_dev), n, c * v, D.ptr(prep), c, k, v, D.ptr(codes), code_bits, 0,
                              D.ptr(near), D.stream_ptr()), "centroid_search_fast")
     return codes
 
@@ -223,6 +223,35 @@ def lut_gather_f32(enc, table):
     err = D.ErrFlag(dev)
     out = _gather_f32(codes, t_dev, None, 0, c, k, m, err.p)
     check(load().lut_read_status(err.p, D.stream_ptr()), "lut_gather_f32")
+    return D.from_device(out, kind)
+
+
+def lut_gather_i32_tc(enc, q):
+    """lut_gather_i32 on the tensor cores (one-hot kind::i8 GEMM, exact int32).
+    Power-of-two K <= 128; codes are range-checked on the host/device first."""
+    qshape = D.shape_of(q)
+    if len(qshape) != 3:
+        raise ShapeError(f"table must be int8 (C, K, M), got {qshape}")
+    c, k, m = qshape
+    _check_enc_shape(enc, c)
+    kind = D.kind_of(enc)
+    dev = D.require_cuda()
+    codes = _codes_device(enc, c, k, dev)
+    n = codes.shape[0]
+    if codes.numel() and int(codes.max()) >= k:
+        raise CorruptionError(f"encoding index {int(codes.max())} >= K={k}")
+    lib = load()
+    if lib.lut_onehot_image_bytes(c, k, m, 1) == 0:
+        raise ConfigError("shape not supported by the tensor-core gather")
+    stride = int(lib.lut_code_stride(c))
+    padded = torch.zeros((n, stride), dtype=torch.uint8, device=dev)
+    padded[:, :c] = codes
+    q_dev = D.to_device(q, np.int8, dev)
+    img = torch.empty(lib.lut_onehot_image_bytes(c, k, m, 1), dtype=torch.uint8, device=dev)
+    check(lib.lut_onehot_prepare_i8(D.ptr(q_dev), c, k, m, img.data_ptr(), D.stream_ptr()), "onehot_prepare_i8")
+    out = torch.empty((n, m), dtype=torch.int32, device=dev)
+    check(lib.lut_gather_onehot(D.ptr(padded), stride, n, c, k, m, 1, img.data_ptr(), None, 0, None, 0, None,
+                                D.ptr(out), 0, D.stream_ptr()), "lut_gather_i32_tc")
     return D.from_device(out, kind)
 
 

@@ -34,9 +34,23 @@ class LutLayer:
     ("relu" / "gelu" fused into the epilogue) and `scale_mtile` (per-m-tile
     int8 scales)."""
 
+    GATHERS = ("auto", "cuda", "tensor")
+
     def __init__(self, cfg: PqConfig, books, weight=None, bias=None, qat: bool = False, table=None,
                  qtable: LookupTableI8 | None = None, trees=None, act=None, scale_mtile: int = 0,
-                 device=None):
+                 device=None, gather: str = "auto", f32_digits: int = 4):
+        """`gather` picks the lookup engine: "cuda" = CUDA-core kernels (f32
+        bitwise ascending-c, int8 exact); "tensor" = tcgen05 one-hot GEMM (int8
+        exact; f32 as `f32_digits` int8 digit planes, within the fp32
+        contract); "auto" = tensor for int8 (bit-identical either way), cuda
+        for f32 (bitwise drop-in)."""
+        if gather not in self.GATHERS:
+            raise ConfigError(f"gather must be one of {self.GATHERS}, got {gather!r}")
+        if f32_digits not in (2, 4):
+            raise ConfigError("f32_digits must be 2 or 4")
+        self.gather = gather
+        self.f32_digits = f32_digits
+        self._images = {}
         self.device = torch.device(device) if device is not None else D.require_cuda()
         books = validate_codebooks(books)
         c, k, v = D.shape_of(books)
@@ -115,7 +129,8 @@ class LutLayer:
             return
         self.table = build_table_device(self.weight, self.books)
         self.qtable = quantize_table(self.table, self.scale_mtile) if self.qat else None
-        self._desc_cache = {} if hasattr(self, "_desc_cache") else None
+        self._desc_cache = {}
+        self._images = {}
 
     def forward_table(self):
         """Table the training forward reads: dequantized under QAT (softpq.py:134-140)."""
@@ -131,8 +146,38 @@ class LutLayer:
             self.scale_mtile = scale_mtile
         self.qtable = quantize_table(self.table, self.scale_mtile)
         self._desc_cache = {}
+        self._images.pop(1, None)
 
     # ---------------------------------------------------------------- ABI
+    def uses_tensor_cores(self, integer: bool) -> bool:
+        if self.gather == "cuda":
+            return False
+        if self.gather == "auto" and not integer:
+            return False
+        digits = 1 if integer else self.f32_digits
+        return load().lut_onehot_image_bytes(self.c, self.k, self.m, digits) > 0
+
+    def onehot_image(self, integer: bool) -> torch.Tensor:
+        """Swizzled tcgen05 B image of the table (built once, lut_onehot_prepare_*)."""
+        digits = 1 if integer else self.f32_digits
+        img = self._images.get(digits)
+        if img is None:
+            lib = load()
+            nbytes = lib.lut_onehot_image_bytes(self.c, self.k, self.m, digits)
+            if nbytes == 0:
+                raise ConfigError("shape not supported by the tensor-core gather")
+            img = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            if integer:
+                check(lib.lut_onehot_prepare_i8(D.ptr(self.qtable.q), self.c, self.k, self.m, img.data_ptr(),
+                                                D.stream_ptr()), "onehot_prepare_i8")
+            else:
+                err = D.ErrFlag(self.device)
+                check(lib.lut_onehot_prepare_f32(D.ptr(self.table), self.c, self.k, self.m, digits, img.data_ptr(),
+                                                 err.p, D.stream_ptr()), "onehot_prepare_f32")
+                check(lib.lut_read_status(err.p, D.stream_ptr()), "onehot_prepare_f32")
+            self._images[digits] = img
+        return img
+
     def desc(self, integer: bool) -> LayerDesc:
         key = bool(integer)
         if key in self._desc_cache:
@@ -149,8 +194,15 @@ class LutLayer:
         d.bias = D.ptr(self.bias)
         d.act = ACTS[self.act]
         d.integer = 1 if integer else 0
+        if self.uses_tensor_cores(integer):
+            d.onehot_image = D.ptr(self.onehot_image(integer))
+            d.onehot_digits = 1 if integer else self.f32_digits
         self._desc_cache[key] = d
         return d
+
+    @property
+    def code_stride(self) -> int:
+        return int(load().lut_code_stride(self.c))
 
     def forward_device(self, a_dev: torch.Tensor, integer: bool, out: torch.Tensor | None = None,
                        codes: torch.Tensor | None = None, near: torch.Tensor | None = None) -> torch.Tensor:
@@ -159,7 +211,7 @@ class LutLayer:
         if out is None:
             out = torch.empty((n, self.m), dtype=torch.float32, device=a_dev.device)
         if codes is None:
-            codes = torch.empty((n, max(self.c, 1)), dtype=torch.uint8, device=a_dev.device)
+            codes = torch.empty((n, self.code_stride), dtype=torch.uint8, device=a_dev.device)
         check(load().lut_layer_forward(C.byref(self.desc(integer)), D.ptr(a_dev), n, D.ptr(out), D.ptr(codes),
                                        D.ptr(near), D.stream_ptr()), "lut_layer_infer")
         return out

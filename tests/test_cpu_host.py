@@ -38,9 +38,9 @@ def test_abi_rejects_bad_geometry_without_gpu():
     from paper_2302_03213_b200 import _lib
 
     h = _lib.load()
-    assert h.lut_encode_f32(None, 10, 7, None, 2, 16, 4, None, 8, None, None) == 2  # d != C*V
-    assert h.lut_encode_f32(None, 10, 8, None, 2, 300, 4, None, 8, None, None) == 2  # K > 256
-    assert h.lut_encode_f32(None, 10, 8, None, 2, 32, 4, None, 4, None, None) == 2  # u4 with K > 16
+    assert h.lut_encode_f32(None, 10, 7, None, 2, 16, 4, None, 8, 0, None, None) == 2  # d != C*V
+    assert h.lut_encode_f32(None, 10, 8, None, 2, 300, 4, None, 8, 0, None, None) == 2  # K > 256
+    assert h.lut_encode_f32(None, 10, 8, None, 2, 32, 4, None, 4, 0, None, None) == 2  # u4 with K > 16
     assert b"4-bit" in h.lut_last_error()
     assert h.lut_gather_f32(None, 8, 5, 2, 16, 4, None, None, 9, None, 0, None, None) == 2  # bad act
     assert h.lut_gather_i8(None, 8, 5, 2, 16, 4, None, None, -1, None, 0, None, None, 0, None, None) == 2

@@ -288,3 +288,63 @@ def test_reference_style_layer_object(L):
     assert got.tobytes() == O.lut_layer_infer(a, books, q=q, scale=s, bias=np.zeros(7, F32)).tobytes()
     got = L.lut_layer_infer(a, ref_layer, integer=False)
     assert got.tobytes() == O.lut_layer_infer(a, books, table=table, bias=np.zeros(7, F32), integer=False).tobytes()
+
+
+# --------------------------------------------------------- tensor-core path
+
+def test_tc_int8_crit1_bitwise(L, golden):
+    """tcgen05 one-hot int8 gather == reference i32 / accumulate, bitwise, on the
+    200 acceptance shapes; f32 digit planes within rtol/atol 1e-5."""
+    meta = golden.cases("crit1")
+    for trial, a, books, b in G.crit1_inputs():
+        case = meta[trial]
+        codes = golden.arrays[f"crit1_codes_{trial}"]
+        table = O.build_table(b, books)
+        q, s = O.quantize_table(table)
+        np.testing.assert_array_equal(L.kernels.lut_gather_i32_tc(codes, q), golden.arrays[f"crit1_i32_{trial}"],
+                                      err_msg=str(trial))
+        layer = L.LutLayer(cfg=L.PqConfig(v=case["v"], k=case["k"]), books=books, weight=b,
+                           bias=np.zeros(case["m"], F32), qat=True, gather="tensor")
+        assert layer.uses_tensor_cores(True) and layer.uses_tensor_cores(False)
+        out8 = L.lut_layer_infer(a, layer, integer=True)
+        want8 = O.lut_gather_accumulate(codes, q, s) + np.zeros(case["m"], F32)
+        assert out8.tobytes() == want8.tobytes(), trial
+        outf = L.lut_layer_infer(a, layer, integer=False)
+        wantf = O.lut_matmul_ref(codes, table)
+        np.testing.assert_allclose(outf, wantf, rtol=1e-5, atol=1e-5, err_msg=str(trial))
+
+
+def test_tc_cfg1(L, golden):
+    case = golden.cases("cfg1")
+    a, books, w = G.cfg1_inputs()
+    layer = L.LutLayer(cfg=L.PqConfig(v=16, k=16), books=books, weight=w, bias=np.zeros(768, F32), qat=True,
+                       gather="tensor")
+    assert G.sha(L.lut_layer_infer(a, layer, integer=True)) == case["out_i8_sha"]
+    table = O.build_table(w, books)
+    want = O.lut_matmul_ref(golden.arrays["cfg1_codes"], table)
+    got = L.lut_layer_infer(a, layer, integer=False)
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-5)
+    # digits=4 is far tighter than the contract: error <= C * max|T| * 2^-31 + f32 rounding
+    assert np.max(np.abs(got.astype(np.float64) - want)) < 2e-6
+
+
+@pytest.mark.parametrize("shape", [(8192, 128, 16, 32, 4096), (5000, 24, 16, 32, 3072), (3000, 96, 16, 32, 768),
+                                   (777, 33, 8, 4, 100), (300, 64, 64, 8, 130), (4096, 128, 64, 32, 512)])
+def test_tc_matches_cuda_core(L, shape):
+    """Tensor-core vs CUDA-core engines on the same device codes: int8 bitwise,
+    f32 within rtol/atol 1e-5 (configs[1] and configs[4] geometries)."""
+    import torch
+
+    n, c, k, v, m = shape
+    g = torch.Generator(device="cuda").manual_seed(n + m)
+    a = torch.randn((n, c * v), generator=g, device="cuda")
+    books = torch.randn((c, k, v), generator=g, device="cuda")
+    w = torch.randn((c * v, m), generator=g, device="cuda") / np.sqrt(c * v)
+    bias = torch.randn(m, generator=g, device="cuda") * 0.1
+    lt = L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=books, weight=w, bias=bias, qat=True, gather="tensor")
+    lc = L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=books, weight=w, bias=bias, qat=True, gather="cuda")
+    assert lt.uses_tensor_cores(True)
+    assert torch.equal(L.lut_layer_infer(a, lt, integer=True), L.lut_layer_infer(a, lc, integer=True))
+    ft = L.lut_layer_infer(a, lt, integer=False)
+    fc = L.lut_layer_infer(a, lc, integer=False)
+    torch.testing.assert_close(ft, fc, rtol=1e-5, atol=1e-5)
