@@ -91,7 +91,7 @@ static EncodeTiledFn encode_tiled_fn() {
 
 static bool make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t cols,
                          uint64_t rows, uint64_t row_stride_bytes, uint32_t box_cols, uint32_t box_rows,
-                         bool swizzle128) {
+                         bool swizzle128, CUtensorMapSwizzle swz_override = CU_TENSOR_MAP_SWIZZLE_NONE) {
   EncodeTiledFn fn = encode_tiled_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
@@ -99,7 +99,7 @@ static bool make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* b
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t elem[2] = {1, 1};
   CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : swz_override,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -109,6 +109,16 @@ bool make_tmap_2d_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_
   if ((cols * 4) % 16 != 0) return false;
   return make_tmap_2d(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, base, cols, rows, cols * 4, box_cols, box_rows,
                       swizzle128);
+}
+
+bool make_tmap_2d_f32_box(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint32_t box_cols,
+                          uint32_t box_rows) {
+  if ((cols * 4) % 16 != 0) return false;
+  CUtensorMapSwizzle swz = box_cols == 32   ? CU_TENSOR_MAP_SWIZZLE_128B
+                           : box_cols == 16 ? CU_TENSOR_MAP_SWIZZLE_64B
+                           : box_cols == 8  ? CU_TENSOR_MAP_SWIZZLE_32B
+                                            : CU_TENSOR_MAP_SWIZZLE_NONE;
+  return make_tmap_2d(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, base, cols, rows, cols * 4, box_cols, box_rows, false, swz);
 }
 
 bool make_tmap_2d_u8(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t row_stride_bytes,

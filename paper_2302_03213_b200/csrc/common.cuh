@@ -30,6 +30,10 @@ size_t max_smem_optin();
 // driver entry point, so the library needs no link-time libcuda dependency.
 bool make_tmap_2d_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
                       uint32_t box_cols, uint32_t box_rows, bool swizzle128);
+// f32 2-D map whose box inner size (floats) picks the matching swizzle:
+// 32 -> 128B, 16 -> 64B, 8 -> 32B, 4 -> none (TMA-store epilogues).
+bool make_tmap_2d_f32_box(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint32_t box_cols,
+                          uint32_t box_rows);
 bool make_tmap_2d_u8(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
                      uint64_t row_stride_bytes, uint32_t box_cols, uint32_t box_rows,
                      bool swizzle128);
@@ -77,8 +81,23 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// try_wait with a suspend-time hint: the waiting thread sleeps until the phase
+// completes (or the hint elapses) instead of spinning on issue slots that the
+// co-resident producer / generator / epilogue warps need.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
+  while (!mbar_try_wait_sleep(bar, parity)) {
   }
 }
 

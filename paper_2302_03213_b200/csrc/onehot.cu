@@ -35,10 +35,10 @@
 
 namespace lutgpu {
 
-constexpr int kOhThreads = 12 * 32;
+constexpr int kOhThreads = 16 * 32;
 constexpr int kRowsPerTile = 128;
 constexpr int kKB = 128;       // K bytes per A stage / B block
-constexpr int kAStages = 4;
+constexpr int kMaxAStages = 12;  // A ring depth: fills TMEM (2*NT accumulator + 32/stage)
 
 struct OneHotParams {
   const uint8_t* b_image;   // [ntiles][nkb][NT][128] swizzled
@@ -60,6 +60,11 @@ struct OneHotParams {
   int64_t out_hw;
   int32_t* out_i32;
   uint32_t tmem_cols;
+  int a_stages;             // A ring depth (<= kMaxAStages)
+  int tma_out;              // 1: epilogue stages the tile in SMEM and TMA-stores it
+  unsigned long long* trace;  // optional per-role cycle counters (LUTGPU_OH_TRACE), CTA 0 only
+  int debug;                // ablation bits (LUTGPU_OH_DEBUG): 1 no epilogue math/stores, 2 no MMA,
+                            // 4 no TMEM A stores, 8 MMA only (no A handshake, generators idle)
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -158,99 +163,171 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
 // ------------------------------------------------------------ work walk
 
 struct UnitWalk {
-  int64_t band, nbands, lo, hi, cur;  // units [lo, hi) of the current band
-  int64_t brt;
-  const OneHotParams* p;
-  __device__ void init(const OneHotParams& pp) {
-    p = &pp;
-    nbands = (pp.nrt + pp.band_rt - 1) / pp.band_rt;
+  // Units of a band are ordered n-tile-major; this CTA owns a contiguous
+  // slice [lo, hi) of each band.  All state is 32-bit and updated
+  // incrementally (no per-unit 64-bit division on the critical path).
+  int band, nbands;
+  int brt;            // row tiles in the current band
+  int left;           // units left in this band's slice
+  int ntile, rtl;     // current position (rtl = row tile inside the band)
+  int nrt, band_rt, ntiles;
+  int slot, nslots;   // this worker (CTA or CTA pair) among all workers
+  __device__ void init(const OneHotParams& pp, int slot_ = -1, int nslots_ = -1) {
+    nrt = (int)pp.nrt;
+    band_rt = (int)pp.band_rt;
+    ntiles = pp.ntiles;
+    slot = slot_ < 0 ? (int)blockIdx.x : slot_;
+    nslots = nslots_ < 0 ? (int)gridDim.x : nslots_;
+    nbands = (nrt + band_rt - 1) / band_rt;
     band = -1;
-    lo = hi = cur = 0;
+    left = 0;
   }
-  // next unit -> (ntile, rt); false at the end
-  __device__ bool next(int& ntile, int64_t& rt) {
-    while (cur >= hi) {
+  __device__ bool next(int& nt, int64_t& rt) {
+    while (left == 0) {
       if (++band >= nbands) return false;
-      brt = min(p->band_rt, p->nrt - band * p->band_rt);
-      const int64_t ub = (int64_t)p->ntiles * brt;
-      lo = ub * blockIdx.x / gridDim.x;
-      hi = ub * (blockIdx.x + 1) / gridDim.x;
-      cur = lo;
+      brt = min(band_rt, nrt - band * band_rt);
+      const int64_t ub = (int64_t)ntiles * brt;
+      const int lo = (int)(ub * slot / nslots);
+      const int hi = (int)(ub * (slot + 1) / nslots);
+      left = hi - lo;
+      ntile = lo / brt;
+      rtl = lo - ntile * brt;
     }
-    ntile = (int)(cur / brt);
-    rt = band * p->band_rt + cur % brt;
-    ++cur;
+    nt = ntile;
+    rt = (int64_t)band * band_rt + rtl;
+    --left;
+    if (++rtl == brt) {
+      rtl = 0;
+      ++ntile;
+    }
     return true;
   }
 };
 
-// ------------------------------------------------------------ one-hot words
+// ------------------------------------------------------------ kernel
 
-// 32 words = one 128-byte K block of this row's one-hot; codes for the block
-// come from the swizzled code tile.  Power-of-two K only (host checks).
+__device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
+  return v;
+}
+
+__device__ __forceinline__ void sts_v4(uint32_t saddr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Code bytes of one ring stage (two 128-byte K blocks) for this row, read
+// from the 128B-swizzled code tile (16-byte chunk j of row r at
+// ((j ^ (r & 7)) << 4), 16 KB per 128-column box).
 template <int K>
-__device__ __forceinline__ void onehot_block(const uint8_t* code_row_sw, int sw, int kb, int C, bool valid,
-                                             uint32_t (&w)[32]) {
-  constexpr int CPB = kKB / K;  // codebooks per block (>= 1 for K <= 128)
-  if constexpr (K >= 4) {
-    constexpr int WPC = K / 4;  // words per codebook
-    const int c0 = kb * CPB;
-    constexpr int NW = (CPB + 3) / 4;
-    uint32_t codes4[NW];
-    // fetch the CPB code bytes from the swizzled tile (aligned words)
+struct StageCodes {
+  static constexpr int CPB = kKB / K;          // codebooks per K block
+  static constexpr int CPS = 2 * CPB;          // codebooks per stage
+  static constexpr int NW = (CPS + 3) / 4;     // code words per stage
+  uint32_t w[NW];
+  __device__ __forceinline__ void load(uint32_t row_saddr, int sw, int st) {
+    const int c0 = st * CPS;
+    if constexpr (NW == 4) {  // 16 code bytes = one aligned chunk
+      const int chunk = c0 >> 4;
+      const uint32_t a = row_saddr + ((chunk >> 3) << 14) + (((chunk & 7) ^ sw) << 4);
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                   : "r"(a));
+    } else {
 #pragma unroll
-    for (int i = 0; i < NW; ++i) {
-      const int byte = (c0 & ~3) + 4 * i;
-      const int chunk = byte >> 4, within = byte & 15;
-      codes4[i] = *reinterpret_cast<const uint32_t*>(code_row_sw + (((chunk & 7) ^ sw) << 4) + ((chunk >> 3) << 14) +
-                                                     within);
-    }
-    if constexpr (CPB < 4) codes4[0] >>= 8 * (c0 & 3);
-#pragma unroll
-    for (int cb = 0; cb < CPB; ++cb) {
-      const uint32_t code = (codes4[cb >> 2] >> (8 * (cb & 3))) & 255u;
-      const bool live = valid && (c0 + cb < C);
-      if constexpr (K == 16) {
-        // one 64-bit shift places the byte; bit 3 of the code picks the half
-        const uint64_t v = live ? (1ull << (8 * (code & 7))) : 0ull;
-        const bool upper = (code & 8) != 0;
-        w[cb * 4 + 0] = upper ? 0u : (uint32_t)v;
-        w[cb * 4 + 1] = upper ? 0u : (uint32_t)(v >> 32);
-        w[cb * 4 + 2] = upper ? (uint32_t)v : 0u;
-        w[cb * 4 + 3] = upper ? (uint32_t)(v >> 32) : 0u;
-      } else {
-        const uint32_t bit = live ? (1u << (8 * (code & 3))) : 0u;
-        const uint32_t wi = code >> 2;
-#pragma unroll
-        for (int j = 0; j < WPC; ++j) w[cb * WPC + j] = (wi == (uint32_t)j) ? bit : 0u;
+      for (int i = 0; i < NW; ++i) {
+        const int byte = (c0 & ~3) + 4 * i;
+        const int chunk = byte >> 4;
+        w[i] = lds_u32(row_saddr + ((chunk >> 3) << 14) + (((chunk & 7) ^ sw) << 4) + (byte & 15));
       }
+      if constexpr (CPS < 4) w[0] >>= 8 * (c0 & 3);
     }
-  } else {
-    // K in {1, 2}: several codebooks per word
+  }
+};
+
+// 1 << s for a 64-bit value with PTX semantics: shift counts >= 64 give 0.
+__device__ __forceinline__ uint64_t shl64(uint32_t s) {
+  uint64_t r;
+  asm("shl.b64 %0, 1, %1;" : "=l"(r) : "r"(s));
+  return r;
+}
+
+// One-hot bytes of a stage: byte (cb*K + code) of the 2*128-byte row is 1.
+// No validity masking: rows >= n are never stored and codebooks >= C meet
+// zero rows of the B image.
+template <int K>
+__device__ __forceinline__ void build_onehot(const StageCodes<K>& cd, uint32_t (&w)[64]) {
+  constexpr int CPS = StageCodes<K>::CPS;
+  constexpr int WPC = K / 4;  // words per codebook
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      uint32_t v = 0;
+  for (int cb = 0; cb < CPS; ++cb) {
+    const uint32_t code = __byte_perm(cd.w[cb >> 2], 0, 0x4440 + (cb & 3)) & (K - 1);
+    if constexpr (K == 16) {
+      const uint64_t lo = shl64(code << 3);          // bytes 0..7   (code < 8)
+      const uint64_t hi = shl64((code << 3) - 64u);  // bytes 8..15  (code >= 8; wraps -> 0 otherwise)
+      w[cb * 4 + 0] = (uint32_t)lo;
+      w[cb * 4 + 1] = (uint32_t)(lo >> 32);
+      w[cb * 4 + 2] = (uint32_t)hi;
+      w[cb * 4 + 3] = (uint32_t)(hi >> 32);
+    } else if constexpr (K == 8) {
+      const uint64_t v = shl64(code << 3);
+      w[cb * 2 + 0] = (uint32_t)v;
+      w[cb * 2 + 1] = (uint32_t)(v >> 32);
+    } else if constexpr (K == 4) {
+      w[cb] = 1u << (code << 3);
+    } else {
+      const uint32_t bit = 1u << ((code & 3) << 3);
+      const uint32_t wi = code >> 2;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int kbyte = kb * kKB + 4 * j + b;
-        const int c = kbyte / K, kk = kbyte % K;
-        if (valid && c < C) {
-          const int chunk = c >> 4, within = c & 15;
-          const uint32_t code =
-              code_row_sw[(((chunk & 7) ^ sw) << 4) + ((chunk >> 3) << 14) + within];
-          if ((int)code == kk) v |= 1u << (8 * b);
-        }
-      }
-      w[j] = v;
+      for (int j = 0; j < WPC; ++j) w[cb * WPC + j] = (wi == (uint32_t)j) ? bit : 0u;
     }
   }
 }
 
-// ------------------------------------------------------------ kernel
+__device__ __forceinline__ void tmem_st64(uint32_t taddr, const uint32_t (&v)[64]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, "
+      "%36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, "
+      "%57, %58, %59, %60, %61, %62, %63, %64};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]),
+      "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]),
+      "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]), "r"(v[32]), "r"(v[33]), "r"(v[34]), "r"(v[35]),
+      "r"(v[36]), "r"(v[37]), "r"(v[38]), "r"(v[39]), "r"(v[40]), "r"(v[41]), "r"(v[42]), "r"(v[43]), "r"(v[44]),
+      "r"(v[45]), "r"(v[46]), "r"(v[47]), "r"(v[48]), "r"(v[49]), "r"(v[50]), "r"(v[51]), "r"(v[52]), "r"(v[53]),
+      "r"(v[54]), "r"(v[55]), "r"(v[56]), "r"(v[57]), "r"(v[58]), "r"(v[59]), "r"(v[60]), "r"(v[61]), "r"(v[62]),
+      "r"(v[63])
+      : "memory");
+}
+
+// cycle accounting for the LUTGPU_OH_TRACE diagnostic (CTA 0, one lane per role)
+#define OH_T0(var) long long var = (p.trace && blockIdx.x == 0) ? clock64() : 0
+#define OH_ACC(slot, var) \
+  do {                    \
+    if (p.trace && blockIdx.x == 0 && lane == 0) atomicAdd(p.trace + (slot), (unsigned long long)(clock64() - var)); \
+  } while (0)
+
+constexpr int kGenWarp0 = 4;   // warps 4..11: generators (parity = (warp-4)>>2)
+constexpr int kEpiWarp0 = 12;  // warps 12..15: epilogue
+constexpr int kGenWarps = 8;
+constexpr int kStageCols = 64;  // TMEM columns per A stage (2 K blocks x 128 B / 4 B)
 
 template <int K, int DIGITS>
 __global__ void __launch_bounds__(kOhThreads, 1)
-    onehot_gemm_kernel(const __grid_constant__ CUtensorMap codes_map, const __grid_constant__ OneHotParams p) {
+    onehot_gemm_kernel(const __grid_constant__ CUtensorMap codes_map, const __grid_constant__ CUtensorMap out_map,
+                       const __grid_constant__ OneHotParams p) {
+  static_assert(K >= 4, "K >= 4 on the tensor-core path");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -258,27 +335,31 @@ __global__ void __launch_bounds__(kOhThreads, 1)
   uint8_t* b_smem = smem;
   const int code_tile_bytes = p.code_boxes * kRowsPerTile * 128;
   uint8_t* code_smem = smem + ((b_bytes + 1023) & ~1023);  // 2 stages
-  uint64_t* bars = reinterpret_cast<uint64_t*>(code_smem + 2 * code_tile_bytes);
+  uint8_t* stage_out = code_smem + 2 * code_tile_bytes;   // 2 x (128 x MT f32) when p.tma_out
+  const int out_tile_bytes = kRowsPerTile * p.MT * 4;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + (p.tma_out ? 2 * out_tile_bytes : 0));
   uint64_t* b_full = bars + 0;
   uint64_t* b_empty = bars + 1;
   uint64_t* code_full = bars + 2;   // [2]
   uint64_t* code_empty = bars + 4;  // [2]
-  uint64_t* a_full = bars + 6;      // [kAStages]
-  uint64_t* a_empty = bars + 6 + kAStages;
-  uint64_t* acc_full = bars + 6 + 2 * kAStages;   // [2]
-  uint64_t* acc_empty = bars + 8 + 2 * kAStages;  // [2]
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(bars + 10 + 2 * kAStages);
+  uint64_t* a_full = bars + 6;      // [kMaxAStages]
+  uint64_t* a_empty = bars + 6 + kMaxAStages;
+  uint64_t* acc_full = bars + 6 + 2 * kMaxAStages;   // [2]
+  uint64_t* acc_empty = bars + 8 + 2 * kMaxAStages;  // [2]
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(bars + 10 + 2 * kMaxAStages);
+  const uint32_t nas = (uint32_t)p.a_stages;
+  const int nst = (p.nkb + 1) >> 1;  // ring stages per unit
 
   if (threadIdx.x == 0) {
     mbar_init(b_full, 1);
     mbar_init(b_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&code_full[i], 1);
-      mbar_init(&code_empty[i], 4);
+      mbar_init(&code_empty[i], kGenWarps);
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], 4);
     }
-    for (int i = 0; i < kAStages; ++i) {
+    for (int i = 0; i < p.a_stages; ++i) {
       mbar_init(&a_full[i], 4);
       mbar_init(&a_empty[i], 1);
     }
@@ -290,10 +371,11 @@ __global__ void __launch_bounds__(kOhThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
   const uint32_t acc_col0 = 0;                    // accumulators: [0, 2*NT)
-  const uint32_t a_col0 = 2 * p.NT;               // A ring: kAStages x 32 columns
+  const uint32_t a_col0 = 2 * p.NT;               // A ring: a_stages x 64 columns
 
   UnitWalk walk;
   walk.init(p);
+  OH_T0(t_kernel);
 
   if (warp == 0) {
     // ------------------------------------------------ producer
@@ -321,7 +403,11 @@ __global__ void __launch_bounds__(kOhThreads, 1)
           }
           cur_ntile = ntile;
         }
-        mbar_wait(&code_empty[cs], cphase ^ 1);
+        {
+          OH_T0(t0);
+          mbar_wait(&code_empty[cs], cphase ^ 1);
+          OH_ACC(10, t0);
+        }
         mbar_arrive_expect_tx(&code_full[cs], (uint32_t)code_tile_bytes);
         for (int bx = 0; bx < p.code_boxes; ++bx)
           tma_load_2d(code_smem + cs * code_tile_bytes + bx * kRowsPerTile * 128, &codes_map, bx * 128,
@@ -337,8 +423,7 @@ __global__ void __launch_bounds__(kOhThreads, 1)
     const uint32_t idesc = idesc_i8(128, p.NT);
     int cur_ntile = -1;
     uint32_t b_phase = 0;
-    int as = 0;
-    uint32_t aphase = 0;
+    uint32_t as = 0, aph = 0;  // A stage / phase of the next ring stage
     int acc = 0;
     uint32_t accphase = 0;
     int ntile;
@@ -347,36 +432,54 @@ __global__ void __launch_bounds__(kOhThreads, 1)
     int nt_next;
     int64_t rt_next;
     bool has_next = look.next(nt_next, rt_next);
+    const uint64_t b_desc0 = sw128_desc(b_smem);
     while (has_next) {
       ntile = nt_next;
       rt = rt_next;
       has_next = look.next(nt_next, rt_next);
       if (ntile != cur_ntile) {
+        OH_T0(t0);
         mbar_wait(b_full, b_phase);
+        OH_ACC(0, t0);
         b_phase ^= 1;
         cur_ntile = ntile;
       }
-      mbar_wait(&acc_empty[acc], accphase ^ 1);
+      {
+        OH_T0(t0);
+        mbar_wait(&acc_empty[acc], accphase ^ 1);
+        OH_ACC(1, t0);
+      }
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc_col0 + acc * p.NT;
-      for (int kb = 0; kb < p.nkb; ++kb) {
-        mbar_wait(&a_full[as], aphase);
+      OH_T0(t_unit);
+      for (int st = 0; st < nst; ++st) {
+        {
+          OH_T0(t0);
+          if (!(p.debug & 8)) mbar_wait(&a_full[as], aph);
+          OH_ACC(2, t0);
+        }
         tc_fence_after();
         if (lane == 0) {
-          const uint8_t* bblk = b_smem + (size_t)kb * p.NT * kKB;
+          const int nk = min(2, p.nkb - 2 * st);
+          for (int kk = 0; kk < nk; ++kk) {
+            const int kb = 2 * st + kk;
+            // descriptor start address advances in 16-byte units: block kb, 32-byte K step j
+            const uint64_t bd = b_desc0 + (uint64_t)((kb * p.NT * kKB) >> 4);
 #pragma unroll
-          for (int j = 0; j < kKB / 32; ++j) {
-            const uint32_t a_tmem = tmem_base + a_col0 + as * 32 + j * 8;
-            mma_i8_ts(d_tmem, a_tmem, sw128_desc(bblk + j * 32), idesc, (kb | j) != 0);
+            for (int j = 0; j < kKB / 32; ++j) {
+              const uint32_t a_tmem = tmem_base + a_col0 + as * kStageCols + kk * 32 + j * 8;
+              if (!(p.debug & 2)) mma_i8_ts(d_tmem, a_tmem, bd + (uint64_t)(j * 2), idesc, (kb | j) != 0);
+            }
           }
           tc_commit(&a_empty[as]);
         }
         __syncwarp();
-        if (++as == kAStages) {
+        if (++as == nas) {
           as = 0;
-          aphase ^= 1;
+          aph ^= 1;
         }
       }
+      OH_ACC(3, t_unit);
       if (lane == 0) {
         tc_commit(&acc_full[acc]);
         if (!has_next || nt_next != ntile) tc_commit(b_empty);
@@ -387,36 +490,65 @@ __global__ void __launch_bounds__(kOhThreads, 1)
         accphase ^= 1;
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= kGenWarp0 && warp < kGenWarp0 + kGenWarps) {
     // ------------------------------------------------ one-hot generators
     const int sub = warp & 3;
+    const int par = (warp - kGenWarp0) >> 2;
     const int row_in_tile = sub * 32 + lane;
     const int sw = row_in_tile & 7;
+    const uint32_t lane_base = tmem_base + ((uint32_t)(sub * 32) << 16) + a_col0;
     int cs = 0;
     uint32_t cphase = 0;
-    int as = 0;
-    uint32_t aphase = 0;
+    // ring stages are dealt to the two warps of a lane group by global index
+    // parity; my_g is this warp's next global stage, (as, aph) its slot.
+    uint32_t unit_g = 0, my_g = (uint32_t)par;
+    uint32_t as = (uint32_t)par % nas, aph = 0;
     int ntile;
     int64_t rt;
+    const bool tr = (warp == kGenWarp0);
     while (walk.next(ntile, rt)) {
-      mbar_wait(&code_full[cs], cphase);
-      const uint8_t* code_row = code_smem + cs * code_tile_bytes + row_in_tile * 128;
-      const bool valid = rt * kRowsPerTile + row_in_tile < p.n;
-      for (int kb = 0; kb < p.nkb; ++kb) {
-        uint32_t w[32];
-        onehot_block<K>(code_row, sw, kb, p.C, valid, w);
-        mbar_wait(&a_empty[as], aphase ^ 1);
+      {
+        OH_T0(t0);
+        mbar_wait(&code_full[cs], cphase);
+        if (tr) OH_ACC(4, t0);
+      }
+      const uint32_t row_saddr = smem_u32(code_smem + cs * code_tile_bytes) + row_in_tile * 128;
+      const uint32_t unit_end = unit_g + nst;
+      if (p.debug & 8) my_g = unit_end + (my_g & 1);  // MMA-only ablation: generators idle
+      StageCodes<K> cur, nxt;
+      if (my_g < unit_end) cur.load(row_saddr, sw, (int)(my_g - unit_g));
+      uint32_t w[64];
+      for (; my_g < unit_end; my_g += 2) {
+        const int st = (int)(my_g - unit_g);
+        if (my_g + 2 < unit_end) nxt.load(row_saddr, sw, st + 2);
+        {
+          OH_T0(t0);
+          build_onehot<K>(cur, w);
+          if (tr) OH_ACC(5, t0);
+        }
+        {
+          OH_T0(t0);
+          mbar_wait(&a_empty[as], aph ^ 1);
+          if (tr) OH_ACC(6, t0);
+        }
         tc_fence_after();
-        tmem_st32(tmem_base + ((uint32_t)(sub * 32) << 16) + a_col0 + as * 32, w);
-        tmem_st_wait();
+        if (!(p.debug & 4)) {
+          OH_T0(t0);
+          tmem_st64(lane_base + as * kStageCols, w);
+          tmem_st_wait();
+          if (tr) OH_ACC(7, t0);
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_full[as]);
-        if (++as == kAStages) {
-          as = 0;
-          aphase ^= 1;
+        cur = nxt;
+        as += 2;
+        if (as >= nas) {
+          as -= nas;
+          aph ^= 1;
         }
       }
+      unit_g = unit_end;
       __syncwarp();
       if (lane == 0) mbar_arrive(&code_empty[cs]);
       if (++cs == 2) {
@@ -424,85 +556,567 @@ __global__ void __launch_bounds__(kOhThreads, 1)
         cphase ^= 1;
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------ epilogue
     const int sub = warp & 3;
     const int row_in_tile = sub * 32 + lane;
+    const bool leader = (warp == kEpiWarp0 && lane == 0);
     int acc = 0;
     uint32_t accphase = 0;
+    int sb = 0;
     int ntile;
     int64_t rt;
+    // swizzle of this row inside a staging box of IB floats (128B/64B/32B/none)
+    const int ib = p.MT < 32 ? p.MT : 32;
+    const int swz = ib == 32 ? (row_in_tile & 7) : ib == 16 ? ((row_in_tile >> 1) & 3) : ib == 8 ? ((row_in_tile >> 2) & 1) : 0;
+    const float scale0 = (DIGITS == 1 && p.scales) ? __ldg(p.scales) : 1.0f;
+    const int ib_log2 = 31 - __clz(ib);
+    const bool tr = (warp == kEpiWarp0);
     while (walk.next(ntile, rt)) {
-      mbar_wait(&acc_full[acc], accphase);
+      {
+        OH_T0(t0);
+        mbar_wait(&acc_full[acc], accphase);
+        if (tr) OH_ACC(8, t0);
+      }
+      OH_T0(t_epi);
       tc_fence_after();
       const int64_t row = rt * kRowsPerTile + row_in_tile;
       const bool live = row < p.n;
       const int m_base = ntile * p.MT;
+      if (p.tma_out) {
+        if (leader) bulk_wait_read1();  // staging buffer sb (used two units ago) is free
+        named_barrier_sync(1, 128);
+      }
+      const uint32_t out_saddr = smem_u32(stage_out + sb * out_tile_bytes);
       for (int ch = 0; ch < p.NT; ch += 16) {
         uint32_t v[16];
         tmem_ld16(tmem_base + ((uint32_t)(sub * 32) << 16) + acc_col0 + acc * p.NT + ch, v);
         tmem_ld_wait();
-        if (!live) continue;
-        constexpr int RC = 16 / DIGITS;  // real columns in this chunk
-        float f[RC];
-#pragma unroll
-        for (int j = 0; j < RC; ++j) {
-          const int m = m_base + (ch / DIGITS) + j;
-          float x;
-          if constexpr (DIGITS == 1) {
-            const int acc_i = (int)v[j];
-            if (p.out_i32 && m < p.M) {
-              const int64_t o = p.out_hw > 0 ? ((row / p.out_hw) * p.M + m) * p.out_hw + row % p.out_hw
-                                             : row * p.M + m;
-              p.out_i32[o] = acc_i;
-            }
-            const float s = (m < p.M && p.scales)
-                                ? (p.scale_mtile > 0 ? __ldg(p.scales + m / p.scale_mtile) : __ldg(p.scales))
-                                : 1.0f;
-            x = __fmul_rn(__int2float_rn(acc_i), s);
-          } else {
-            long long t = 0;
-#pragma unroll
-            for (int dg = DIGITS - 1; dg >= 0; --dg) t = t * 256 + (long long)(int)v[j * DIGITS + dg];
-            const double s = m < p.M ? __ldg(p.col_scale + m) : 0.0;
-            x = (float)((double)t * s);
-          }
-          if (p.bias && m < p.M) x = __fadd_rn(x, __ldg(p.bias + m));
-          f[j] = apply_act(x, p.act);
+        if (ch + 16 >= p.NT) {
+          // all accumulator columns are in registers: hand TMEM back to the MMA
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[acc]);
         }
-        if (p.out) {
-          const int m0 = m_base + ch / DIGITS;
-          if (p.out_hw == 0 && m0 + RC <= p.M && (p.M & 3) == 0 && (RC & 3) == 0) {
-            float4* dst = reinterpret_cast<float4*>(p.out + row * p.M + m0);
-#pragma unroll
-            for (int j = 0; j < RC / 4; ++j) dst[j] = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
-          } else {
+        if (p.debug & 1) continue;
+        constexpr int RC = 16 / DIGITS;  // real columns in this chunk
+        const int mc = m_base + ch / DIGITS;  // first real column of the chunk
+        const bool full_chunk = mc + RC <= p.M;
+        float f[RC];
+        if constexpr (DIGITS == 1) {
+          if (p.out_i32 && live) {
 #pragma unroll
             for (int j = 0; j < RC; ++j) {
-              const int m = m0 + j;
+              const int m = mc + j;
               if (m < p.M) {
                 const int64_t o = p.out_hw > 0 ? ((row / p.out_hw) * p.M + m) * p.out_hw + row % p.out_hw
                                                : row * p.M + m;
-                p.out[o] = f[j];
+                p.out_i32[o] = (int)v[j];
               }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < RC; ++j) {
+            const int m = mc + j;
+            const float s = p.scale_mtile > 0 ? (m < p.M ? __ldg(p.scales + m / p.scale_mtile) : 1.0f) : scale0;
+            f[j] = __fmul_rn(__int2float_rn((int)v[j]), s);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < RC; ++j) {
+            long long t = 0;
+#pragma unroll
+            for (int dg = DIGITS - 1; dg >= 0; --dg) t = t * 256 + (long long)(int)v[j * DIGITS + dg];
+            const int m = mc + j;
+            const double s = m < p.M ? __ldg(p.col_scale + m) : 0.0;
+            f[j] = (float)((double)t * s);
+          }
+        }
+        if (p.bias) {
+          if (full_chunk && (RC % 4) == 0 && ((mc & 3) == 0)) {
+#pragma unroll
+            for (int j = 0; j < RC; j += 4) {
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + mc + j));
+              f[j] = __fadd_rn(f[j], b4.x);
+              f[j + 1] = __fadd_rn(f[j + 1], b4.y);
+              f[j + 2] = __fadd_rn(f[j + 2], b4.z);
+              f[j + 3] = __fadd_rn(f[j + 3], b4.w);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < RC; ++j)
+              if (mc + j < p.M) f[j] = __fadd_rn(f[j], __ldg(p.bias + mc + j));
+          }
+        }
+        if (p.act) {
+#pragma unroll
+          for (int j = 0; j < RC; ++j) f[j] = apply_act(f[j], p.act);
+        }
+        if (!p.out) continue;
+        const int ml0 = ch / DIGITS;  // first real column (tile-local) of this chunk
+        if (p.tma_out) {
+#pragma unroll
+          for (int j = 0; j < RC / 4; ++j) {
+            const int ml = ml0 + 4 * j;
+            const int box = ml >> ib_log2, within = ml & (ib - 1);
+            const int chunk = (within >> 2) ^ swz;
+            sts_v4(out_saddr + box * (kRowsPerTile * ib * 4) + row_in_tile * (ib * 4) + (chunk << 4), f[4 * j],
+                   f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+          }
+        } else if (live) {
+#pragma unroll
+          for (int j = 0; j < RC; ++j) {
+            const int m = m_base + ml0 + j;
+            if (m < p.M) {
+              const int64_t o = p.out_hw > 0 ? ((row / p.out_hw) * p.M + m) * p.out_hw + row % p.out_hw
+                                             : row * p.M + m;
+              p.out[o] = f[j];
             }
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      if (p.tma_out && p.out && !(p.debug & 1)) {
+        fence_proxy_async_smem();
+        named_barrier_sync(1, 128);
+        if (leader) {
+          for (int bx = 0; bx < p.MT / ib; ++bx)
+            tma_store_2d(&out_map, stage_out + sb * out_tile_bytes + bx * (kRowsPerTile * ib * 4), m_base + bx * ib,
+                         (int32_t)(rt * kRowsPerTile));
+          bulk_commit();
+        }
+        sb ^= 1;
+      }
+      if (tr) OH_ACC(9, t_epi);
       if (++acc == 2) {
         acc = 0;
         accphase ^= 1;
       }
     }
+    if (leader) bulk_wait_all();
   }
+  if (warp == 1) OH_ACC(11, t_kernel);
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+}
+
+// ------------------------------------------------------------ CTA-pair kernel
+//
+// Same pipeline, but two CTAs of a cluster issue ONE tcgen05.mma.cta_group::2
+// (M = 256 rows, N = 2 x 64 columns): each SM keeps half of the B image tile
+// (64 columns, SMEM) and generates the one-hot A of its own 128 rows into its
+// own TMEM; each SM's accumulator is its 128 rows x all N columns.  N = 128 is
+// what the kind::i8 pipe needs to run at its full 8192 MAC/clk/SM (N = 64
+// single-CTA MMAs are issue-bound at ~70%), and it halves the one-hot
+// generation per output column.  The leader CTA's elected thread issues the
+// MMAs; generators / epilogue / producer of the peer arrive on the leader's
+// barriers through DSMEM; MMA completion is multicast-committed to both CTAs.
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// arrive on an mbarrier given by its shared::cluster address (may be the peer's)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait_cluster(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  // arrive on the barrier at this offset in both CTAs of the pair
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+template <int K, int DIGITS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
+    onehot_pair_kernel(const __grid_constant__ CUtensorMap codes_map, const __grid_constant__ CUtensorMap out_map,
+                       const __grid_constant__ OneHotParams p) {
+  static_assert(K >= 4, "K >= 4 on the tensor-core path");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int NH = p.NT;        // B rows held by this CTA (half of the MMA N)
+  const int NN = 2 * p.NT;    // MMA N = accumulator columns
+  const int b_bytes = NH * p.nkb * kKB;
+  uint8_t* b_smem = smem;
+  const int code_tile_bytes = p.code_boxes * kRowsPerTile * 128;
+  uint8_t* code_smem = smem + ((b_bytes + 1023) & ~1023);  // 2 stages
+  uint8_t* stage_out = code_smem + 2 * code_tile_bytes;   // 2 x half-unit staging when p.tma_out
+  const int MTU = NN / DIGITS;                             // real output columns per unit
+  const int half_cols = MTU / 2;                           // real columns per epilogue half
+  const int half_bytes = kRowsPerTile * half_cols * 4;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + (p.tma_out ? 2 * half_bytes : 0));
+  uint64_t* b_full = bars + 0;      // local: own half landed
+  uint64_t* b_empty = bars + 1;     // multicast commit: MMAs done with B
+  uint64_t* code_full = bars + 2;   // [2] local
+  uint64_t* code_empty = bars + 4;  // [2] local
+  uint64_t* a_full = bars + 6;      // [kMaxAStages] leader: 8 generator warps (4 local + 4 peer)
+  uint64_t* a_empty = bars + 6 + kMaxAStages;          // multicast commit
+  uint64_t* acc_full = bars + 6 + 2 * kMaxAStages;     // [2] multicast commit
+  uint64_t* acc_empty = bars + 8 + 2 * kMaxAStages;    // [2] leader: 8 epilogue warps
+  uint64_t* b_ready = bars + 10 + 2 * kMaxAStages;     // leader: peer's B half landed
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(bars + 11 + 2 * kMaxAStages);
+  const uint32_t nas = (uint32_t)p.a_stages;
+  const int nst = (p.nkb + 1) >> 1;
+
+  if (threadIdx.x == 0) {
+    mbar_init(b_full, 1);
+    mbar_init(b_empty, 1);
+    mbar_init(b_ready, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&code_full[i], 1);
+      mbar_init(&code_empty[i], kGenWarps);
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 8);
+    }
+    for (int i = 0; i < p.a_stages; ++i) {
+      mbar_init(&a_full[i], 8);
+      mbar_init(&a_empty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_smem)),
+                 "r"(p.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised before any remote arrive
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_smem;
+  const uint32_t a_col0 = 2 * NN;  // accumulators: [0, 2*NN); A ring after
+
+  UnitWalk walk;
+  walk.init(p, (int)(blockIdx.x >> 1), (int)(gridDim.x >> 1));
+  // leader-side barrier addresses seen from this CTA
+  const uint32_t a_full_l = map_to_rank(smem_u32(a_full), 0);
+  const uint32_t acc_empty_l = map_to_rank(smem_u32(acc_empty), 0);
+  const uint32_t b_ready_l = map_to_rank(smem_u32(b_ready), 0);
+
+  if (warp == 0) {
+    // ------------------------------------------------ producer (both CTAs)
+    if (lane == 0) {
+      prefetch_tmap(&codes_map);
+      int cur_ntile = -1;
+      uint32_t b_phase = 0, bf_phase = 0;
+      int cs = 0;
+      uint32_t cphase = 0;
+      int ntile;
+      int64_t rt;
+      bool first_b = true;
+      while (walk.next(ntile, rt)) {
+        if (ntile != cur_ntile) {
+          if (!first_b) {
+            mbar_wait(b_empty, b_phase);
+            b_phase ^= 1;
+          }
+          first_b = false;
+          mbar_arrive_expect_tx(b_full, (uint32_t)b_bytes);
+          const uint8_t* src = p.b_image + (size_t)(2 * ntile + (int)rank) * b_bytes;
+          for (int off = 0; off < b_bytes; off += 32768) {
+            const int chunk = min(32768, b_bytes - off);
+            bulk_load(b_smem + off, src + off, (uint32_t)chunk, b_full);
+          }
+          if (!leader) {  // tell the leader's MMA issuer once our half has landed
+            mbar_wait(b_full, bf_phase);
+            bf_phase ^= 1;
+            mbar_arrive_cluster(b_ready_l);
+          }
+          cur_ntile = ntile;
+        }
+        mbar_wait(&code_empty[cs], cphase ^ 1);
+        mbar_arrive_expect_tx(&code_full[cs], (uint32_t)code_tile_bytes);
+        for (int bx = 0; bx < p.code_boxes; ++bx)
+          tma_load_2d(code_smem + cs * code_tile_bytes + bx * kRowsPerTile * 128, &codes_map, bx * 128,
+                      (int32_t)(rt * 2 * kRowsPerTile + rank * kRowsPerTile), &code_full[cs]);
+        if (++cs == 2) {
+          cs = 0;
+          cphase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (leader only)
+    if (leader) {
+      const uint32_t idesc = idesc_i8(256, NN);
+      int cur_ntile = -1;
+      uint32_t b_phase = 0;
+      uint32_t as = 0, aph = 0;
+      int acc = 0;
+      uint32_t accphase = 0;
+      int ntile;
+      int64_t rt;
+      UnitWalk look = walk;
+      int nt_next;
+      int64_t rt_next;
+      bool has_next = look.next(nt_next, rt_next);
+      const uint64_t b_desc0 = sw128_desc(b_smem);
+      while (has_next) {
+        ntile = nt_next;
+        rt = rt_next;
+        has_next = look.next(nt_next, rt_next);
+        if (ntile != cur_ntile) {
+          mbar_wait(b_full, b_phase);
+          mbar_wait_cluster(b_ready, b_phase);
+          b_phase ^= 1;
+          cur_ntile = ntile;
+        }
+        mbar_wait_cluster(&acc_empty[acc], accphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * NN;
+        for (int st = 0; st < nst; ++st) {
+          mbar_wait_cluster(&a_full[as], aph);
+          tc_fence_after();
+          if (lane == 0) {
+            const int nk = min(2, p.nkb - 2 * st);
+            for (int kk = 0; kk < nk; ++kk) {
+              const int kb = 2 * st + kk;
+              const uint64_t bd = b_desc0 + (uint64_t)((kb * NH * kKB) >> 4);
+              const uint32_t ab = tmem_base + a_col0 + as * kStageCols + kk * 32;
+#pragma unroll
+              for (int j = 0; j < kKB / 32; ++j)
+                if (!(p.debug & 2)) mma_i8_ts_pair(d_tmem, ab + j * 8, bd + (uint64_t)(j * 2), idesc, (kb | j) != 0);
+            }
+            tc_commit_pair(&a_empty[as]);
+          }
+          __syncwarp();
+          if (++as == nas) {
+            as = 0;
+            aph ^= 1;
+          }
+        }
+        if (lane == 0) {
+          tc_commit_pair(&acc_full[acc]);
+          if (!has_next || nt_next != ntile) tc_commit_pair(b_empty);
+        }
+        __syncwarp();
+        if (++acc == 2) {
+          acc = 0;
+          accphase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= kGenWarp0 && warp < kGenWarp0 + kGenWarps) {
+    // ------------------------------------------------ one-hot generators (both CTAs)
+    const int sub = warp & 3;
+    const int par = (warp - kGenWarp0) >> 2;
+    const int row_in_tile = sub * 32 + lane;
+    const int sw = row_in_tile & 7;
+    const uint32_t lane_base = tmem_base + ((uint32_t)(sub * 32) << 16) + a_col0;
+    int cs = 0;
+    uint32_t cphase = 0;
+    uint32_t unit_g = 0, my_g = (uint32_t)par;
+    uint32_t as = (uint32_t)par % nas, aph = 0;
+    int ntile;
+    int64_t rt;
+    while (walk.next(ntile, rt)) {
+      mbar_wait(&code_full[cs], cphase);
+      const uint32_t row_saddr = smem_u32(code_smem + cs * code_tile_bytes) + row_in_tile * 128;
+      const uint32_t unit_end = unit_g + nst;
+      StageCodes<K> cur, nxt;
+      if (my_g < unit_end) cur.load(row_saddr, sw, (int)(my_g - unit_g));
+      uint32_t w[64];
+      for (; my_g < unit_end; my_g += 2) {
+        const int st = (int)(my_g - unit_g);
+        if (my_g + 2 < unit_end) nxt.load(row_saddr, sw, st + 2);
+        build_onehot<K>(cur, w);
+        mbar_wait(&a_empty[as], aph ^ 1);
+        tc_fence_after();
+        if (!(p.debug & 4)) {
+          tmem_st64(lane_base + as * kStageCols, w);
+          tmem_st_wait();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(a_full_l + as * 8);
+        cur = nxt;
+        as += 2;
+        if (as >= nas) {
+          as -= nas;
+          aph ^= 1;
+        }
+      }
+      unit_g = unit_end;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&code_empty[cs]);
+      if (++cs == 2) {
+        cs = 0;
+        cphase ^= 1;
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ------------------------------------------------ epilogue (both CTAs)
+    const int sub = warp & 3;
+    const int row_in_tile = sub * 32 + lane;
+    const bool elected = (warp == kEpiWarp0 && lane == 0);
+    int acc = 0;
+    uint32_t accphase = 0;
+    int ntile;
+    int64_t rt;
+    const int ib = half_cols < 32 ? half_cols : 32;
+    const int ib_log2 = 31 - __clz(ib);
+    const int swz = ib == 32 ? (row_in_tile & 7) : ib == 16 ? ((row_in_tile >> 1) & 3) : ib == 8 ? ((row_in_tile >> 2) & 1) : 0;
+    const float scale0 = (DIGITS == 1 && p.scales) ? __ldg(p.scales) : 1.0f;
+    while (walk.next(ntile, rt)) {
+      mbar_wait(&acc_full[acc], accphase);
+      tc_fence_after();
+      const int64_t row0 = rt * 2 * kRowsPerTile + rank * kRowsPerTile;
+      const int64_t row = row0 + row_in_tile;
+      const bool live = row < p.n;
+      const int m_base = ntile * MTU;
+      for (int hf = 0; hf < 2; ++hf) {
+        if (p.tma_out) {
+          if (elected) bulk_wait_read1();  // staging half hf (used one unit ago) is free
+          named_barrier_sync(1, 128);
+        }
+        const uint32_t out_saddr = smem_u32(stage_out + hf * half_bytes);
+        for (int ch = hf * (NN / 2); ch < (hf + 1) * (NN / 2); ch += 16) {
+          uint32_t v[16];
+          tmem_ld16(tmem_base + ((uint32_t)(sub * 32) << 16) + acc * NN + ch, v);
+          tmem_ld_wait();
+          if (ch + 16 >= NN) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(acc_empty_l + acc * 8);
+          }
+          if (p.debug & 1) continue;
+          constexpr int RC = 16 / DIGITS;
+          const int mc = m_base + ch / DIGITS;
+          const bool full_chunk = mc + RC <= p.M;
+          float f[RC];
+          if constexpr (DIGITS == 1) {
+            if (p.out_i32 && live) {
+#pragma unroll
+              for (int j = 0; j < RC; ++j) {
+                const int m = mc + j;
+                if (m < p.M)
+                  p.out_i32[p.out_hw > 0 ? ((row / p.out_hw) * p.M + m) * p.out_hw + row % p.out_hw : row * p.M + m] =
+                      (int)v[j];
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < RC; ++j) {
+              const int m = mc + j;
+              const float s = p.scale_mtile > 0 ? (m < p.M ? __ldg(p.scales + m / p.scale_mtile) : 1.0f) : scale0;
+              f[j] = __fmul_rn(__int2float_rn((int)v[j]), s);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < RC; ++j) {
+              long long t = 0;
+#pragma unroll
+              for (int dg = DIGITS - 1; dg >= 0; --dg) t = t * 256 + (long long)(int)v[j * DIGITS + dg];
+              const int m = mc + j;
+              const double s = m < p.M ? __ldg(p.col_scale + m) : 0.0;
+              f[j] = (float)((double)t * s);
+            }
+          }
+          if (p.bias) {
+            if (full_chunk && (RC % 4) == 0 && ((mc & 3) == 0)) {
+#pragma unroll
+              for (int j = 0; j < RC; j += 4) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + mc + j));
+                f[j] = __fadd_rn(f[j], b4.x);
+                f[j + 1] = __fadd_rn(f[j + 1], b4.y);
+                f[j + 2] = __fadd_rn(f[j + 2], b4.z);
+                f[j + 3] = __fadd_rn(f[j + 3], b4.w);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < RC; ++j)
+                if (mc + j < p.M) f[j] = __fadd_rn(f[j], __ldg(p.bias + mc + j));
+            }
+          }
+          if (p.act) {
+#pragma unroll
+            for (int j = 0; j < RC; ++j) f[j] = apply_act(f[j], p.act);
+          }
+          if (!p.out) continue;
+          const int ml0 = (ch - hf * (NN / 2)) / DIGITS;  // column inside this half
+          if (p.tma_out) {
+#pragma unroll
+            for (int j = 0; j < RC / 4; ++j) {
+              const int ml = ml0 + 4 * j;
+              const int box = ml >> ib_log2, within = ml & (ib - 1);
+              const int chunk = (within >> 2) ^ swz;
+              sts_v4(out_saddr + box * (kRowsPerTile * ib * 4) + row_in_tile * (ib * 4) + (chunk << 4), f[4 * j],
+                     f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+            }
+          } else if (live) {
+#pragma unroll
+            for (int j = 0; j < RC; ++j) {
+              const int m = mc + j;
+              if (m < p.M)
+                p.out[p.out_hw > 0 ? ((row / p.out_hw) * p.M + m) * p.out_hw + row % p.out_hw : row * p.M + m] = f[j];
+            }
+          }
+        }
+        if (p.tma_out && p.out && !(p.debug & 1)) {
+          fence_proxy_async_smem();
+          named_barrier_sync(1, 128);
+          if (elected) {
+            for (int bx = 0; bx < half_cols / ib; ++bx)
+              tma_store_2d(&out_map, stage_out + hf * half_bytes + bx * (kRowsPerTile * ib * 4),
+                           m_base + hf * half_cols + bx * ib, (int32_t)row0);
+            bulk_commit();
+          }
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        accphase ^= 1;
+      }
+    }
+    if (elected) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no remote arrive may target a CTA that has left
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols)
+                 : "memory");
   }
 }
 
@@ -576,11 +1190,12 @@ __global__ void bimg_digits_kernel(const float* __restrict__ t, int C, int K, in
 // ------------------------------------------------------------ host
 
 struct OneHotGeom {
-  int NT, MT, ntiles, nkb;
+  int NT, MT, ntiles, nkb;  // NT/MT/ntiles describe B image tiles (one CTA's B)
+  bool pair;                // CTA-pair kernel: MMA N = 2*NT, image tiles paired
   size_t img_bytes;
 };
 
-static bool pow2_k(int K) { return K >= 1 && K <= 128 && (K & (K - 1)) == 0; }
+static bool pow2_k(int K) { return K >= 4 && K <= 128 && (K & (K - 1)) == 0; }
 
 static OneHotGeom onehot_geom(int C, int K, int M, int digits) {
   OneHotGeom g{};
@@ -590,9 +1205,17 @@ static OneHotGeom onehot_geom(int C, int K, int M, int digits) {
   while (NT > 16 && (size_t)NT * g.nkb * kKB > budget) NT /= 2;
   // do not waste B rows on a small M
   while (NT > 16 && NT / 2 >= M * digits) NT /= 2;
+  {
+    const char* e = getenv("LUTGPU_OH_NT");  // tuning override (smaller only)
+    if (e && atoi(e) >= 16 && atoi(e) < NT && (atoi(e) & 15) == 0) NT = atoi(e);
+  }
   g.NT = NT;
   g.MT = NT / digits;
   g.ntiles = (M + g.MT - 1) / g.MT;
+  // N <= 64 per SM leaves the i8 MMA issue-bound: pair two SMs (N = 2*NT)
+  const char* e = getenv("LUTGPU_OH_PAIR");
+  g.pair = NT <= 64 && (NT >= 32 || digits == 1) && !(e && e[0] == '0');
+  if (g.pair && (g.ntiles & 1)) ++g.ntiles;  // image tiles come in pairs (zero padded)
   g.img_bytes = (size_t)g.ntiles * NT * g.nkb * kKB;
   return g;
 }
@@ -648,27 +1271,52 @@ const double* onehot_col_scale(const void* image, int C, int K, int M, int digit
 }
 
 template <int K, int DIGITS>
-static int launch_onehot_k(const CUtensorMap& map, OneHotParams& p, size_t smem, int grid, cudaStream_t stream) {
+static int launch_onehot_k(const CUtensorMap& map, const CUtensorMap& omap, OneHotParams& p, size_t smem, int grid,
+                           cudaStream_t stream) {
   auto kern = onehot_gemm_kernel<K, DIGITS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(onehot)");
-  kern<<<grid, kOhThreads, smem, stream>>>(map, p);
+  kern<<<grid, kOhThreads, smem, stream>>>(map, omap, p);
   LUT_CHECK_LAUNCH("onehot_gemm_kernel");
   return LUT_OK;
 }
 
+template <int K, int DIGITS>
+static int launch_pair_k(const CUtensorMap& map, const CUtensorMap& omap, OneHotParams& p, size_t smem, int grid,
+                         cudaStream_t stream) {
+  auto kern = onehot_pair_kernel<K, DIGITS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(onehot_pair)");
+  kern<<<grid, kOhThreads, smem, stream>>>(map, omap, p);
+  LUT_CHECK_LAUNCH("onehot_pair_kernel");
+  return LUT_OK;
+}
+
 template <int DIGITS>
-static int dispatch_k(int K, const CUtensorMap& map, OneHotParams& p, size_t smem, int grid, cudaStream_t stream) {
+static int dispatch_pair(int K, const CUtensorMap& map, const CUtensorMap& omap, OneHotParams& p, size_t smem,
+                         int grid, cudaStream_t stream) {
   switch (K) {
-    case 1: return launch_onehot_k<1, DIGITS>(map, p, smem, grid, stream);
-    case 2: return launch_onehot_k<2, DIGITS>(map, p, smem, grid, stream);
-    case 4: return launch_onehot_k<4, DIGITS>(map, p, smem, grid, stream);
-    case 8: return launch_onehot_k<8, DIGITS>(map, p, smem, grid, stream);
-    case 16: return launch_onehot_k<16, DIGITS>(map, p, smem, grid, stream);
-    case 32: return launch_onehot_k<32, DIGITS>(map, p, smem, grid, stream);
-    case 64: return launch_onehot_k<64, DIGITS>(map, p, smem, grid, stream);
-    case 128: return launch_onehot_k<128, DIGITS>(map, p, smem, grid, stream);
-    default: return fail(LUT_ERR_CONFIG, "one-hot gather needs power-of-two K <= 128");
+    case 4: return launch_pair_k<4, DIGITS>(map, omap, p, smem, grid, stream);
+    case 8: return launch_pair_k<8, DIGITS>(map, omap, p, smem, grid, stream);
+    case 16: return launch_pair_k<16, DIGITS>(map, omap, p, smem, grid, stream);
+    case 32: return launch_pair_k<32, DIGITS>(map, omap, p, smem, grid, stream);
+    case 64: return launch_pair_k<64, DIGITS>(map, omap, p, smem, grid, stream);
+    case 128: return launch_pair_k<128, DIGITS>(map, omap, p, smem, grid, stream);
+    default: return fail(LUT_ERR_CONFIG, "one-hot gather needs power-of-two 4 <= K <= 128");
+  }
+}
+
+template <int DIGITS>
+static int dispatch_k(int K, const CUtensorMap& map, const CUtensorMap& omap, OneHotParams& p, size_t smem, int grid,
+                      cudaStream_t stream) {
+  switch (K) {
+    case 4: return launch_onehot_k<4, DIGITS>(map, omap, p, smem, grid, stream);
+    case 8: return launch_onehot_k<8, DIGITS>(map, omap, p, smem, grid, stream);
+    case 16: return launch_onehot_k<16, DIGITS>(map, omap, p, smem, grid, stream);
+    case 32: return launch_onehot_k<32, DIGITS>(map, omap, p, smem, grid, stream);
+    case 64: return launch_onehot_k<64, DIGITS>(map, omap, p, smem, grid, stream);
+    case 128: return launch_onehot_k<128, DIGITS>(map, omap, p, smem, grid, stream);
+    default: return fail(LUT_ERR_CONFIG, "one-hot gather needs power-of-two 4 <= K <= 128");
   }
 }
 
@@ -706,10 +1354,73 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
   p.out = out;
   p.out_hw = out_hw;
   p.out_i32 = out_i32;
-  uint32_t cols = 2 * g.NT + kAStages * 32;
+  {
+    const char* dbg = getenv("LUTGPU_OH_DEBUG");
+    p.debug = dbg ? atoi(dbg) : 0;
+  }
+  if (g.pair) {
+    // ---------------- CTA-pair kernel: MMA N = 2*NT, 256-row pair tiles
+    const int NN = 2 * g.NT;
+    p.ntiles = g.ntiles / 2;
+    p.MT = NN / digits;
+    p.nrt = (n + 2 * kRowsPerTile - 1) / (2 * kRowsPerTile);
+    p.a_stages = (512 - 2 * NN) / 64;
+    if (p.a_stages > kMaxAStages) p.a_stages = kMaxAStages;
+    if (p.a_stages < 2) return fail(LUT_ERR_CONFIG, "one-hot gather: TMEM budget exceeded");
+    uint32_t alloc = 32;
+    while (alloc < (uint32_t)(2 * NN + p.a_stages * 64)) alloc <<= 1;
+    p.tmem_cols = alloc;
+    const int nsm = num_sms();
+    const int64_t units = (int64_t)p.ntiles * p.nrt;
+    const int pairs = (int)(units < nsm / 2 ? units : nsm / 2);
+    int64_t a = pairs, b = p.ntiles;
+    while (b) {
+      const int64_t t = a % b;
+      a = b;
+      b = t;
+    }
+    p.band_rt = pairs / a;
+    if (p.band_rt < 1) p.band_rt = 1;
+    if (p.band_rt > p.nrt) p.band_rt = p.nrt;
+    const size_t b_bytes = (size_t)g.NT * g.nkb * kKB;
+    const size_t base_smem =
+        ((b_bytes + 1023) & ~size_t(1023)) + 2 * (size_t)code_boxes * kRowsPerTile * 128 + 256 + 1024;
+    if (base_smem > max_smem_optin()) return fail(LUT_ERR_CONFIG, "one-hot gather: shared memory budget exceeded");
+    const int half_cols = p.MT / 2;
+    const int ib = half_cols < 32 ? half_cols : 32;
+    const size_t stage_bytes = 2 * (size_t)kRowsPerTile * half_cols * 4;
+    CUtensorMap omap;
+    memset(&omap, 0, sizeof(omap));
+    p.tma_out = 0;
+    if (out && out_hw == 0 && (M % 4) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && ib >= 4 &&
+        half_cols % ib == 0 && base_smem + stage_bytes <= max_smem_optin()) {
+      if (make_tmap_2d_f32_box(&omap, out, (uint64_t)M, (uint64_t)n, (uint32_t)ib, kRowsPerTile)) p.tma_out = 1;
+    }
+    const size_t smem = base_smem + (p.tma_out ? stage_bytes : 0);
+    p.trace = nullptr;
+    switch (digits) {
+      case 1: return dispatch_pair<1>(K, map, omap, p, smem, 2 * pairs, stream);
+      case 2: return dispatch_pair<2>(K, map, omap, p, smem, 2 * pairs, stream);
+      case 4: return dispatch_pair<4>(K, map, omap, p, smem, 2 * pairs, stream);
+      default: return fail(LUT_ERR_CONFIG, "digits must be 1, 2 or 4");
+    }
+  }
+  // TMEM: 2 accumulators (2*NT columns) + the A ring (64 columns per stage)
+  p.a_stages = (512 - 2 * g.NT) / 64;
+  if (p.a_stages > kMaxAStages) p.a_stages = kMaxAStages;
+  if (p.a_stages < 2) return fail(LUT_ERR_CONFIG, "one-hot gather: TMEM budget exceeded");
+  {
+    const char* st = getenv("LUTGPU_OH_ASTAGES");
+    if (st && atoi(st) >= 2 && atoi(st) <= p.a_stages) p.a_stages = atoi(st);
+  }
+  uint32_t cols = 2 * g.NT + p.a_stages * 64;
   uint32_t alloc = 32;
   while (alloc < cols) alloc <<= 1;
   p.tmem_cols = alloc;
+  {
+    const char* dbg = getenv("LUTGPU_OH_DEBUG");
+    p.debug = dbg ? atoi(dbg) : 0;
+  }
   const int nsm = num_sms();
   const int64_t units = (int64_t)g.ntiles * p.nrt;
   const int grid = (int)(units < nsm ? units : nsm);
@@ -724,12 +1435,49 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
   if (p.band_rt < 1) p.band_rt = 1;
   if (p.band_rt > p.nrt) p.band_rt = p.nrt;
   const size_t b_bytes = (size_t)g.NT * g.nkb * kKB;
-  const size_t smem = ((b_bytes + 1023) & ~size_t(1023)) + 2 * (size_t)code_boxes * kRowsPerTile * 128 + 256 + 1024;
-  if (smem > max_smem_optin()) return fail(LUT_ERR_CONFIG, "one-hot gather: shared memory budget exceeded");
+  const size_t base_smem =
+      ((b_bytes + 1023) & ~size_t(1023)) + 2 * (size_t)code_boxes * kRowsPerTile * 128 + 256 + 1024;
+  if (base_smem > max_smem_optin()) return fail(LUT_ERR_CONFIG, "one-hot gather: shared memory budget exceeded");
+  // TMA-store epilogue: row-major f32 out, 16-byte row pitch, staging fits
+  const size_t stage_bytes = 2 * (size_t)kRowsPerTile * g.MT * 4;
+  CUtensorMap omap;
+  memset(&omap, 0, sizeof(omap));
+  p.tma_out = 0;
+  const int ib = g.MT < 32 ? g.MT : 32;
+  if (out && out_hw == 0 && (M % 4) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && ib >= 4 &&
+      base_smem + stage_bytes <= max_smem_optin()) {
+    if (make_tmap_2d_f32_box(&omap, out, (uint64_t)M, (uint64_t)n, (uint32_t)ib, kRowsPerTile))
+      p.tma_out = 1;
+  }
+  const size_t smem = base_smem + (p.tma_out ? stage_bytes : 0);
+  unsigned long long* trace = nullptr;
+  if (getenv("LUTGPU_OH_TRACE")) {
+    cudaMalloc(&trace, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(trace, 0, 16 * sizeof(unsigned long long), stream);
+  }
+  p.trace = trace;
+  struct TracePrint {
+    unsigned long long* t;
+    cudaStream_t s;
+    int units;
+    ~TracePrint() {
+      if (!t) return;
+      unsigned long long h[16];
+      cudaStreamSynchronize(s);
+      cudaMemcpy(h, t, sizeof(h), cudaMemcpyDeviceToHost);
+      const char* names[12] = {"mma.wait_b",   "mma.wait_acc_empty", "mma.wait_a_full", "mma.unit_total",
+                               "gen.wait_code", "gen.build",         "gen.wait_a_empty", "gen.st",
+                               "epi.wait_acc", "epi.work",          "prod.wait_code_empty", "kernel"};
+      fprintf(stderr, "[onehot trace CTA0, %d units]", units);
+      for (int i = 0; i < 12; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)h[i] / units);
+      fprintf(stderr, " (cycles per unit)\n");
+      cudaFree(t);
+    }
+  } tp{trace, stream, (int)((units + grid - 1) / grid)};
   switch (digits) {
-    case 1: return dispatch_k<1>(K, map, p, smem, grid, stream);
-    case 2: return dispatch_k<2>(K, map, p, smem, grid, stream);
-    case 4: return dispatch_k<4>(K, map, p, smem, grid, stream);
+    case 1: return dispatch_k<1>(K, map, omap, p, smem, grid, stream);
+    case 2: return dispatch_k<2>(K, map, omap, p, smem, grid, stream);
+    case 4: return dispatch_k<4>(K, map, omap, p, smem, grid, stream);
     default: return fail(LUT_ERR_CONFIG, "digits must be 1, 2 or 4");
   }
 }
