@@ -138,6 +138,39 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "memory");
 }
 
+template <int OFF>
+__device__ __forceinline__ void tmem_ld32_at(uint32_t taddr, uint32_t (&v)[64]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[OFF + 0]), "=r"(v[OFF + 1]), "=r"(v[OFF + 2]), "=r"(v[OFF + 3]), "=r"(v[OFF + 4]), "=r"(v[OFF + 5]),
+        "=r"(v[OFF + 6]), "=r"(v[OFF + 7]), "=r"(v[OFF + 8]), "=r"(v[OFF + 9]), "=r"(v[OFF + 10]), "=r"(v[OFF + 11]),
+        "=r"(v[OFF + 12]), "=r"(v[OFF + 13]), "=r"(v[OFF + 14]), "=r"(v[OFF + 15]), "=r"(v[OFF + 16]),
+        "=r"(v[OFF + 17]), "=r"(v[OFF + 18]), "=r"(v[OFF + 19]), "=r"(v[OFF + 20]), "=r"(v[OFF + 21]),
+        "=r"(v[OFF + 22]), "=r"(v[OFF + 23]), "=r"(v[OFF + 24]), "=r"(v[OFF + 25]), "=r"(v[OFF + 26]),
+        "=r"(v[OFF + 27]), "=r"(v[OFF + 28]), "=r"(v[OFF + 29]), "=r"(v[OFF + 30]), "=r"(v[OFF + 31])
+      : "r"(taddr)
+      : "memory");
+}
+
+template <int OFF>
+__device__ __forceinline__ void tmem_ld16_at(uint32_t taddr, uint32_t (&v)[64]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(v[OFF + 0]), "=r"(v[OFF + 1]), "=r"(v[OFF + 2]), "=r"(v[OFF + 3]), "=r"(v[OFF + 4]), "=r"(v[OFF + 5]),
+        "=r"(v[OFF + 6]), "=r"(v[OFF + 7]), "=r"(v[OFF + 8]), "=r"(v[OFF + 9]), "=r"(v[OFF + 10]), "=r"(v[OFF + 11]),
+        "=r"(v[OFF + 12]), "=r"(v[OFF + 13]), "=r"(v[OFF + 14]), "=r"(v[OFF + 15])
+      : "r"(taddr)
+      : "memory");
+}
+
+// exact int32 -> f32 for |x| < 2^22 on the FMA/ALU pipes (I2F is quarter rate):
+// the float with bits 0x4B400000 + x is 12582912 + x exactly.
+__device__ __forceinline__ float i2f_exact(uint32_t x) {
+  return __fsub_rn(__int_as_float(0x4B400000 + (int)x), 12582912.0f);
+}
+
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // SMEM matrix descriptor: K-major, 128B swizzle, 8-row atoms 1024 B apart.
@@ -765,6 +798,60 @@ __device__ __forceinline__ void mma_i8_ts_pair(uint32_t d_tmem, uint32_t a_tmem,
       : "memory");
 }
 
+// One ring stage (up to two 128-byte K blocks = 8 MMAs) issued from a single
+// asm block executed by the whole warp, predicated on elect.sync: operands stay
+// warp-uniform (no per-MMA R2UR/ELECT loop in SASS) and the 8 address offsets
+// are immediates.  acc0 = accumulate flag of the stage's first MMA.
+#define OH_MMA_G(G, AOFF, BOFF, PRED)       \
+  "add.u32 ta, %1, " #AOFF ";\n\t"        \
+  "add.u64 tb, %2, " #BOFF ";\n\t"        \
+  "@e tcgen05.mma.cta_group::" #G ".kind::i8 [%0], [ta], tb, %4, " #PRED ";\n\t"
+#define OH_MMA_H(G, AOFF, BOFF)             \
+  "add.u32 ta, %1, " #AOFF ";\n\t"        \
+  "add.u64 tb, tb2, " #BOFF ";\n\t"       \
+  "@e tcgen05.mma.cta_group::" #G ".kind::i8 [%0], [ta], tb, %4, pt2;\n\t"
+#define OH_STAGE_ASM(G)                                                                      \
+  "{\n\t.reg .pred e, p0, pt2, e2;\n\t.reg .b32 ta;\n\t.reg .b64 tb, tb2;\n\t"            \
+  "elect.sync _|e, 0xffffffff;\n\t"                                                         \
+  "setp.ne.u32 p0, %5, 0;\n\t"                                                              \
+  "setp.eq.u32 pt2, %4, %4;\n\t"                                                            \
+  OH_MMA_G(G, 0, 0, p0) OH_MMA_G(G, 8, 2, pt2) OH_MMA_G(G, 16, 4, pt2) OH_MMA_G(G, 24, 6, pt2) \
+  "setp.ne.u32 e2, %6, 0;\n\t"                                                              \
+  "and.pred e, e, e2;\n\t"                                                                  \
+  "add.u64 tb2, %2, %3;\n\t"                                                                \
+  OH_MMA_H(G, 32, 0) OH_MMA_H(G, 40, 2) OH_MMA_H(G, 48, 4) OH_MMA_H(G, 56, 6) "}"
+
+// One ring stage (up to two 128-byte K blocks = 8 MMAs) issued from a single
+// asm block executed by the whole warp, predicated on elect.sync: operands stay
+// warp-uniform (no per-MMA R2UR/ELECT loop in SASS) and the 8 address offsets
+// are immediates.  acc0 = accumulate flag of the stage's first MMA; two = the
+// stage holds a second K block.
+template <int CG>
+__device__ __forceinline__ void issue_stage(uint32_t d, uint32_t a, uint64_t b, uint64_t bstep, uint32_t idesc,
+                                            uint32_t acc0, uint32_t two) {
+  if constexpr (CG == 2) {
+    asm volatile(OH_STAGE_ASM(2)::"r"(d), "r"(a), "l"(b), "l"(bstep), "r"(idesc), "r"(acc0), "r"(two) : "memory");
+  } else {
+    asm volatile(OH_STAGE_ASM(1)::"r"(d), "r"(a), "l"(b), "l"(bstep), "r"(idesc), "r"(acc0), "r"(two) : "memory");
+  }
+}
+
+// tcgen05.commit from an elected lane (whole warp executes it)
+__device__ __forceinline__ void commit_elect(uint64_t* bar, bool pair) {
+  if (pair)
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
 template <int K, int DIGITS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
     onehot_pair_kernel(const __grid_constant__ CUtensorMap codes_map, const __grid_constant__ CUtensorMap out_map,
@@ -807,10 +894,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
       mbar_init(&code_full[i], 1);
       mbar_init(&code_empty[i], kGenWarps);
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 8);
+      mbar_init(&acc_empty[i], 5);  // 4 leader epilogue warps + 1 arrive for the peer's 4
     }
     for (int i = 0; i < p.a_stages; ++i) {
-      mbar_init(&a_full[i], 8);
+      mbar_init(&a_full[i], 5);     // 4 leader generator warps + 1 arrive for the peer's 4
       mbar_init(&a_empty[i], 1);
     }
     fence_mbar_init();
@@ -825,6 +912,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
   cluster_sync();  // barriers of both CTAs initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
+  if (tmem_base != 0) __trap();  // 512-column allocation must start at column 0
   const uint32_t a_col0 = 2 * NN;  // accumulators: [0, 2*NN); A ring after
 
   UnitWalk walk;
@@ -892,45 +980,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
       int64_t rt_next;
       bool has_next = look.next(nt_next, rt_next);
       const uint64_t b_desc0 = sw128_desc(b_smem);
+      const uint64_t bstep = (uint64_t)((NH * kKB) >> 4);  // descriptor step of one 128-byte K block
       while (has_next) {
         ntile = nt_next;
         rt = rt_next;
         has_next = look.next(nt_next, rt_next);
         if (ntile != cur_ntile) {
+          OH_T0(t0);
           mbar_wait(b_full, b_phase);
           mbar_wait_cluster(b_ready, b_phase);
+          OH_ACC(0, t0);
           b_phase ^= 1;
           cur_ntile = ntile;
         }
-        mbar_wait_cluster(&acc_empty[acc], accphase ^ 1);
+        {
+          OH_T0(t0);
+          mbar_wait_cluster(&acc_empty[acc], accphase ^ 1);
+          OH_ACC(1, t0);
+        }
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * NN;
+        const uint32_t d_tmem = acc * NN;  // TMEM base is column 0: this CTA owns all 512 columns
+        OH_T0(t_unit);
         for (int st = 0; st < nst; ++st) {
-          mbar_wait_cluster(&a_full[as], aph);
-          tc_fence_after();
-          if (lane == 0) {
-            const int nk = min(2, p.nkb - 2 * st);
-            for (int kk = 0; kk < nk; ++kk) {
-              const int kb = 2 * st + kk;
-              const uint64_t bd = b_desc0 + (uint64_t)((kb * NH * kKB) >> 4);
-              const uint32_t ab = tmem_base + a_col0 + as * kStageCols + kk * 32;
-#pragma unroll
-              for (int j = 0; j < kKB / 32; ++j)
-                if (!(p.debug & 2)) mma_i8_ts_pair(d_tmem, ab + j * 8, bd + (uint64_t)(j * 2), idesc, (kb | j) != 0);
-            }
-            tc_commit_pair(&a_empty[as]);
+          {
+            OH_T0(t0);
+            mbar_wait_cluster(&a_full[as], aph);
+            OH_ACC(2, t0);
           }
-          __syncwarp();
+          tc_fence_after();
+          if (!(p.debug & 2))
+            issue_stage<2>(d_tmem, a_col0 + as * kStageCols, b_desc0 + (uint64_t)((2 * st * NH * kKB) >> 4),
+                           bstep, idesc, st != 0, 2 * st + 1 < p.nkb);
+          commit_elect(&a_empty[as], true);
           if (++as == nas) {
             as = 0;
             aph ^= 1;
           }
         }
-        if (lane == 0) {
-          tc_commit_pair(&acc_full[acc]);
-          if (!has_next || nt_next != ntile) tc_commit_pair(b_empty);
-        }
-        __syncwarp();
+        OH_ACC(3, t_unit);
+        commit_elect(&acc_full[acc], true);
+        if (!has_next || nt_next != ntile) commit_elect(b_empty, true);
         if (++acc == 2) {
           acc = 0;
           accphase ^= 1;
@@ -950,8 +1039,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
     uint32_t as = (uint32_t)par % nas, aph = 0;
     int ntile;
     int64_t rt;
+    const bool tr = (warp == kGenWarp0);
+    const int tslot = leader ? 0 : 8;
     while (walk.next(ntile, rt)) {
-      mbar_wait(&code_full[cs], cphase);
+      {
+        long long t0 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
+        mbar_wait(&code_full[cs], cphase);
+        if (tr && p.trace && blockIdx.x < 2 && lane == 0) atomicAdd(p.trace + 4 + tslot, (unsigned long long)(clock64() - t0));
+      }
       const uint32_t row_saddr = smem_u32(code_smem + cs * code_tile_bytes) + row_in_tile * 128;
       const uint32_t unit_end = unit_g + nst;
       StageCodes<K> cur, nxt;
@@ -960,16 +1055,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
       for (; my_g < unit_end; my_g += 2) {
         const int st = (int)(my_g - unit_g);
         if (my_g + 2 < unit_end) nxt.load(row_saddr, sw, st + 2);
+        long long t0 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
         build_onehot<K>(cur, w);
+        long long t1 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
         mbar_wait(&a_empty[as], aph ^ 1);
+        long long t2 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
         tc_fence_after();
         if (!(p.debug & 4)) {
           tmem_st64(lane_base + as * kStageCols, w);
           tmem_st_wait();
         }
+        long long t3 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
+        if (tr && p.trace && blockIdx.x < 2 && lane == 0) {
+          atomicAdd(p.trace + 5 + tslot, (unsigned long long)(t1 - t0));
+          atomicAdd(p.trace + 6 + tslot, (unsigned long long)(t2 - t1));
+          atomicAdd(p.trace + 7 + tslot, (unsigned long long)(t3 - t2));
+        }
         tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(a_full_l + as * 8);
+        if (leader) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&a_full[as]);
+        } else {
+          // the peer's 4 warps of this parity meet locally; one remote arrive
+          named_barrier_sync(2 + par, 128);
+          if (sub == 0 && lane == 0) mbar_arrive_cluster(a_full_l + as * 8);
+        }
         cur = nxt;
         as += 2;
         if (as >= nas) {
@@ -1006,23 +1116,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
       const bool live = row < p.n;
       const int m_base = ntile * MTU;
       for (int hf = 0; hf < 2; ++hf) {
-        if (p.tma_out) {
-          if (elected) bulk_wait_read1();  // staging half hf (used one unit ago) is free
-          named_barrier_sync(1, 128);
-        }
-        const uint32_t out_saddr = smem_u32(stage_out + hf * half_bytes);
-        for (int ch = hf * (NN / 2); ch < (hf + 1) * (NN / 2); ch += 16) {
-          uint32_t v[16];
-          tmem_ld16(tmem_base + ((uint32_t)(sub * 32) << 16) + acc * NN + ch, v);
-          tmem_ld_wait();
-          if (ch + 16 >= NN) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(acc_empty_l + acc * 8);
+        const int HC = NN / 2;  // accumulator columns of this half (16, 32 or 64)
+        uint32_t v[64];
+        {
+          const uint32_t tb = tmem_base + ((uint32_t)(sub * 32) << 16) + acc * NN + hf * HC;
+          if (HC >= 32) {
+            tmem_ld32_at<0>(tb, v);
+            if (HC == 64) tmem_ld32_at<32>(tb + 32, v);
+          } else {
+            tmem_ld16_at<0>(tb, v);
           }
-          if (p.debug & 1) continue;
+          tmem_ld_wait();
+        }
+        if (hf == 1) {
+          // the whole accumulator is in registers: hand it back to the MMA issuer
+          tc_fence_before();
+          if (leader) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[acc]);
+          } else {
+            named_barrier_sync(4, 128);
+            if (elected) mbar_arrive_cluster(acc_empty_l + acc * 8);
+          }
+        }
+        if (p.debug & 1) continue;
+        // each warp stages and TMA-stores its own 32-row slab (box {ib, 32})
+        if (p.tma_out) {
+          if (lane == 0) bulk_wait_read1();  // this warp's slab of half hf (one unit ago) is free
+          __syncwarp();
+        }
+        const uint32_t out_saddr = smem_u32(stage_out + hf * half_bytes) + row_in_tile * (ib * 4);
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) {
+          const int ch = c4 * 16;
+          if (ch >= HC) break;
           constexpr int RC = 16 / DIGITS;
-          const int mc = m_base + ch / DIGITS;
+          const int mc = m_base + (hf * HC + ch) / DIGITS;
           const bool full_chunk = mc + RC <= p.M;
           float f[RC];
           if constexpr (DIGITS == 1) {
@@ -1032,24 +1161,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
                 const int m = mc + j;
                 if (m < p.M)
                   p.out_i32[p.out_hw > 0 ? ((row / p.out_hw) * p.M + m) * p.out_hw + row % p.out_hw : row * p.M + m] =
-                      (int)v[j];
+                      (int)v[ch + j];
               }
             }
+            if (p.scale_mtile > 0) {
 #pragma unroll
-            for (int j = 0; j < RC; ++j) {
-              const int m = mc + j;
-              const float s = p.scale_mtile > 0 ? (m < p.M ? __ldg(p.scales + m / p.scale_mtile) : 1.0f) : scale0;
-              f[j] = __fmul_rn(__int2float_rn((int)v[j]), s);
+              for (int j = 0; j < RC; ++j) {
+                const int m = mc + j;
+                f[j] = __fmul_rn(__int2float_rn((int)v[ch + j]), m < p.M ? __ldg(p.scales + m / p.scale_mtile) : 1.0f);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < RC; ++j) f[j] = __fmul_rn(i2f_exact(v[ch + j]), scale0);
             }
           } else {
 #pragma unroll
             for (int j = 0; j < RC; ++j) {
               long long t = 0;
 #pragma unroll
-              for (int dg = DIGITS - 1; dg >= 0; --dg) t = t * 256 + (long long)(int)v[j * DIGITS + dg];
+              for (int dg = DIGITS - 1; dg >= 0; --dg) t = t * 256 + (long long)(int)v[ch + j * DIGITS + dg];
               const int m = mc + j;
-              const double s = m < p.M ? __ldg(p.col_scale + m) : 0.0;
-              f[j] = (float)((double)t * s);
+              const double sc = m < p.M ? __ldg(p.col_scale + m) : 0.0;
+              f[j] = (float)((double)t * sc);
             }
           }
           if (p.bias) {
@@ -1072,16 +1205,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
 #pragma unroll
             for (int j = 0; j < RC; ++j) f[j] = apply_act(f[j], p.act);
           }
-          if (!p.out) continue;
-          const int ml0 = (ch - hf * (NN / 2)) / DIGITS;  // column inside this half
+          if (!p.out || (p.debug & 32)) {
+            if (p.debug & 32) {  // keep the math alive for the ablation
+              float sacc = 0.f;
+#pragma unroll
+              for (int j = 0; j < RC; ++j) sacc += f[j];
+              if (sacc == 1234.5f) p.out[0] = sacc;
+            }
+            continue;
+          }
+          const int ml0 = ch / DIGITS;  // real column inside this half
           if (p.tma_out) {
 #pragma unroll
             for (int j = 0; j < RC / 4; ++j) {
               const int ml = ml0 + 4 * j;
               const int box = ml >> ib_log2, within = ml & (ib - 1);
               const int chunk = (within >> 2) ^ swz;
-              sts_v4(out_saddr + box * (kRowsPerTile * ib * 4) + row_in_tile * (ib * 4) + (chunk << 4), f[4 * j],
-                     f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+              sts_v4(out_saddr + box * (kRowsPerTile * ib * 4) + (chunk << 4), f[4 * j], f[4 * j + 1], f[4 * j + 2],
+                     f[4 * j + 3]);
             }
           } else if (live) {
 #pragma unroll
@@ -1092,13 +1233,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
             }
           }
         }
-        if (p.tma_out && p.out && !(p.debug & 1)) {
+        if (p.tma_out && p.out && !(p.debug & 48)) {
           fence_proxy_async_smem();
-          named_barrier_sync(1, 128);
-          if (elected) {
+          __syncwarp();
+          if (lane == 0) {
             for (int bx = 0; bx < half_cols / ib; ++bx)
-              tma_store_2d(&out_map, stage_out + hf * half_bytes + bx * (kRowsPerTile * ib * 4),
-                           m_base + hf * half_cols + bx * ib, (int32_t)row0);
+              tma_store_2d(&out_map, stage_out + hf * half_bytes + bx * (kRowsPerTile * ib * 4) + sub * 32 * (ib * 4),
+                           m_base + hf * half_cols + bx * ib, (int32_t)(row0 + sub * 32));
             bulk_commit();
           }
         }
@@ -1108,7 +1249,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
         accphase ^= 1;
       }
     }
-    if (elected) bulk_wait_all();
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -1394,10 +1535,33 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
     p.tma_out = 0;
     if (out && out_hw == 0 && (M % 4) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && ib >= 4 &&
         half_cols % ib == 0 && base_smem + stage_bytes <= max_smem_optin()) {
-      if (make_tmap_2d_f32_box(&omap, out, (uint64_t)M, (uint64_t)n, (uint32_t)ib, kRowsPerTile)) p.tma_out = 1;
+      if (make_tmap_2d_f32_box(&omap, out, (uint64_t)M, (uint64_t)n, (uint32_t)ib, 32)) p.tma_out = 1;
     }
     const size_t smem = base_smem + (p.tma_out ? stage_bytes : 0);
     p.trace = nullptr;
+    if (getenv("LUTGPU_OH_TRACE")) {
+      cudaMalloc(&p.trace, 16 * sizeof(unsigned long long));
+      cudaMemsetAsync(p.trace, 0, 16 * sizeof(unsigned long long), stream);
+    }
+    struct PairTrace {
+      unsigned long long* t;
+      cudaStream_t s;
+      int units;
+      ~PairTrace() {
+        if (!t) return;
+        unsigned long long h[16];
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h, t, sizeof(h), cudaMemcpyDeviceToHost);
+        const char* names[16] = {"L.mma.wait_b", "L.mma.wait_acc_empty", "L.mma.wait_a_full", "L.mma.unit",
+                                 "L.gen.wait_code", "L.gen.build", "L.gen.wait_a_empty", "L.gen.st",
+                                 "-", "-", "-", "-", "P.gen.wait_code", "P.gen.build", "P.gen.wait_a_empty", "P.gen.st"};
+        fprintf(stderr, "[pair trace, %d units]", units);
+        for (int i = 0; i < 16; ++i)
+          if (names[i][0] != '-') fprintf(stderr, " %s=%.0f", names[i], (double)h[i] / units);
+        fprintf(stderr, " (cycles per unit)\n");
+        cudaFree(t);
+      }
+    } ptr{p.trace, stream, (int)((units + pairs - 1) / pairs)};
     switch (digits) {
       case 1: return dispatch_pair<1>(K, map, omap, p, smem, 2 * pairs, stream);
       case 2: return dispatch_pair<2>(K, map, omap, p, smem, 2 * pairs, stream);
