@@ -352,7 +352,8 @@ __device__ __forceinline__ void tmem_st64(uint32_t taddr, const uint32_t (&v)[64
   } while (0)
 
 constexpr int kGenWarp0 = 4;   // warps 4..11: generators (parity = (warp-4)>>2)
-constexpr int kEpiWarp0 = 12;  // warps 12..15: epilogue
+constexpr int kEpiWarp0 = 12;  // warps 12..15: epilogue (pair kernel: 12..19, one accumulator half each)
+constexpr int kPairThreads = 20 * 32;
 constexpr int kGenWarps = 8;
 constexpr int kStageCols = 64;  // TMEM columns per A stage (2 K blocks x 128 B / 4 B)
 
@@ -853,7 +854,7 @@ __device__ __forceinline__ void commit_elect(uint64_t* bar, bool pair) {
 }
 
 template <int K, int DIGITS>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     onehot_pair_kernel(const __grid_constant__ CUtensorMap codes_map, const __grid_constant__ CUtensorMap out_map,
                        const __grid_constant__ OneHotParams p) {
   static_assert(K >= 4, "K >= 4 on the tensor-core path");
@@ -894,7 +895,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
       mbar_init(&code_full[i], 1);
       mbar_init(&code_empty[i], kGenWarps);
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 5);  // 4 leader epilogue warps + 1 arrive for the peer's 4
+      mbar_init(&acc_empty[i], 9);  // 8 leader epilogue warps + 1 arrive for the peer's 8
     }
     for (int i = 0; i < p.a_stages; ++i) {
       mbar_init(&a_full[i], 5);     // 4 leader generator warps + 1 arrive for the peer's 4
@@ -1115,7 +1116,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
       const int64_t row = row0 + row_in_tile;
       const bool live = row < p.n;
       const int m_base = ntile * MTU;
-      for (int hf = 0; hf < 2; ++hf) {
+      {
+        const int hf = (warp - kEpiWarp0) >> 2;  // this warp's accumulator half
         const int HC = NN / 2;  // accumulator columns of this half (16, 32 or 64)
         uint32_t v[64];
         {
@@ -1128,14 +1130,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOhThreads, 1)
           }
           tmem_ld_wait();
         }
-        if (hf == 1) {
-          // the whole accumulator is in registers: hand it back to the MMA issuer
+        {
+          // this warp's half of the accumulator is in registers: release it
           tc_fence_before();
           if (leader) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[acc]);
           } else {
-            named_barrier_sync(4, 128);
+            named_barrier_sync(4, 256);
             if (elected) mbar_arrive_cluster(acc_empty_l + acc * 8);
           }
         }
@@ -1428,7 +1430,7 @@ static int launch_pair_k(const CUtensorMap& map, const CUtensorMap& omap, OneHot
   auto kern = onehot_pair_kernel<K, DIGITS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(onehot_pair)");
-  kern<<<grid, kOhThreads, smem, stream>>>(map, omap, p);
+  kern<<<grid, kPairThreads, smem, stream>>>(map, omap, p);
   LUT_CHECK_LAUNCH("onehot_pair_kernel");
   return LUT_OK;
 }
