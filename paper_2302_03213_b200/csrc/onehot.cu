@@ -1141,7 +1141,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             if (elected) mbar_arrive_cluster(acc_empty_l + acc * 8);
           }
         }
-        if (p.debug & 1) continue;
+        if (!(p.debug & 1)) {
         // each warp stages and TMA-stores its own 32-row slab (box {ib, 32})
         if (p.tma_out) {
           if (lane == 0) bulk_wait_read1();  // this warp's slab of half hf (one unit ago) is free
@@ -1245,6 +1245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             bulk_commit();
           }
         }
+        }  // !(debug & 1)
       }
       if (++acc == 2) {
         acc = 0;
