@@ -38,7 +38,7 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--table", choices=["f32", "i8"], default="f32")
+    p.add_argument("--table", choices=["f32", "i8"], default="i8")
     p.add_argument("--k", type=int, default=16)
     p.add_argument("--rows", type=int, default=1 << 20, help="rows per GPU")
     p.add_argument("--dim", type=int, default=4096)

@@ -64,6 +64,26 @@ __global__ void prepare_books_kernel(const float* __restrict__ books, int C, int
   }
 }
 
+// packed-pair FP32 (sm_100 FFMA2 / FADD2): two lanes of math per issue slot
+__device__ __forceinline__ uint64_t pack_f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack_f2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 __device__ __forceinline__ float tau_coef(int v) { return (4.0f * v + 16.0f) * 5.9604645e-8f; }
 
 // Literal f64 re-decision (encode_hard semantics) for one (row, codebook).
@@ -87,11 +107,14 @@ __device__ __noinline__ int exact_argmin(GetA get_a, const float* __restrict__ c
 
 // --------------------------------------------------------------- TMA path
 
-constexpr int kEncWarps = 8;                  // consumer warps
+constexpr int kEncWarps = 8;                  // consumer warps; a broadcast LDS.128 of a centroid costs
+                                              // 4 SMEM wavefronts, so each feeds kRPL rows
 constexpr int kEncThreads = (kEncWarps + 1) * 32;
 constexpr int kBoxRows = 256;                 // TMA box rows
 constexpr int kRPL = 2;                       // rows per lane
-constexpr int kTileRows = kBoxRows * kRPL;    // 512
+constexpr int kRowsPerPass = kEncWarps * 32;  // rows covered by one pass of all consumer lanes
+constexpr int kTileRows = kRowsPerPass * kRPL;  // 512
+constexpr int kTileBoxes = kTileRows / kBoxRows;  // A boxes per stage
 constexpr int kBoxBytes = kBoxRows * 128;     // 32 KB (32 f32 columns)
 
 struct EncTmaParams {
@@ -108,6 +131,7 @@ struct EncTmaParams {
   int* near_tie;
   int stages;
   int stage_bytes;
+  int debug;  // LUTGPU_ENC_DEBUG: 1 = consumers skip the distance math (TMA streaming only)
 };
 
 __device__ __forceinline__ void store_code_group(uint8_t* dst, uint32_t w0, uint32_t w1,
@@ -134,7 +158,7 @@ __global__ void __launch_bounds__(kEncThreads, 1)
   constexpr int NB = 32 / V;   // codebooks per 32-column box
   constexpr int NJ = V / 4;    // 16-byte chunks per sub-vector
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window (LDS, not generic LD)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * p.stage_bytes);
   uint64_t* empty = full + p.stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -168,12 +192,12 @@ __global__ void __launch_bounds__(kEncThreads, 1)
           uint8_t* st = smem + (size_t)stage * p.stage_bytes;
           const int nsub = min(NB, p.C - b * NB);
           const uint32_t book_bytes = (uint32_t)nsub * p.S * 4;
-          mbar_arrive_expect_tx(&full[stage], kRPL * kBoxBytes + book_bytes);
+          mbar_arrive_expect_tx(&full[stage], kTileBoxes * kBoxBytes + book_bytes);
 #pragma unroll
-          for (int r = 0; r < kRPL; ++r)
+          for (int r = 0; r < kTileBoxes; ++r)
             tma_load_2d(st + r * kBoxBytes, &tmap, b * 32, (int32_t)(tile * kTileRows + r * kBoxRows),
                         &full[stage]);
-          bulk_load(st + kRPL * kBoxBytes, p.prep + (size_t)b * NB * p.S, book_bytes, &full[stage]);
+          bulk_load(st + kTileBoxes * kBoxBytes, p.prep + (size_t)b * NB * p.S, book_bytes, &full[stage]);
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
@@ -187,7 +211,7 @@ __global__ void __launch_bounds__(kEncThreads, 1)
   // ---------------- consumers
   int stage = 0;
   uint32_t phase = 0;
-  const int rr = warp * 32 + lane;  // row within each 256-row box
+  const int rr = warp * 32 + lane;  // this lane's first row in the tile (then + kRowsPerPass)
   const int sw = rr & 7;            // 128B swizzle phase of this row
   const float tau_c = tau_coef(V);
   for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -205,17 +229,19 @@ __global__ void __launch_bounds__(kEncThreads, 1)
     for (int b = b0; b < b1; ++b) {
       mbar_wait(&full[stage], phase);
       const uint8_t* st = smem + (size_t)stage * p.stage_bytes;
-      const float* cent_all = reinterpret_cast<const float*>(st + kRPL * kBoxBytes);
+      const float* cent_all = reinterpret_cast<const float*>(st + kTileBoxes * kBoxBytes);
 #pragma unroll
       for (int sb = 0; sb < NB; ++sb) {
         const int c = b * NB + sb;
-        if (c >= c_end) break;
+        if (c >= c_end || (p.debug & 1)) break;
         const float* cb = cent_all + sb * p.S;
-        float a[kRPL][V];
+        // packed pairs (-2 a_j, -2 a_j+1): FFMA2 does two FMAs per issue slot
+        uint64_t a2[kRPL][V / 2];
         float asq[kRPL];
 #pragma unroll
         for (int r = 0; r < kRPL; ++r) {
-          const float* rowp = reinterpret_cast<const float*>(st + r * kBoxBytes + rr * 128);
+          const int q_ = rr + r * kRowsPerPass;
+          const float* rowp = reinterpret_cast<const float*>(st + (q_ >> 8) * kBoxBytes + (q_ & 255) * 128);
           asq[r] = 0.0f;
 #pragma unroll
           for (int j = 0; j < NJ; ++j) {
@@ -224,10 +250,8 @@ __global__ void __launch_bounds__(kEncThreads, 1)
             asq[r] = fmaf(x.y, x.y, asq[r]);
             asq[r] = fmaf(x.z, x.z, asq[r]);
             asq[r] = fmaf(x.w, x.w, asq[r]);
-            a[r][4 * j + 0] = -2.0f * x.x;
-            a[r][4 * j + 1] = -2.0f * x.y;
-            a[r][4 * j + 2] = -2.0f * x.z;
-            a[r][4 * j + 3] = -2.0f * x.w;
+            a2[r][2 * j + 0] = pack_f2(-2.0f * x.x, -2.0f * x.y);
+            a2[r][2 * j + 1] = pack_f2(-2.0f * x.z, -2.0f * x.w);
           }
         }
         float best[kRPL], second[kRPL];
@@ -239,31 +263,33 @@ __global__ void __launch_bounds__(kEncThreads, 1)
           bi[r] = 0;
         }
         const float* norms = cb + p.K * V;
+        const uint32_t cb_s = smem_u32(cb);
 #pragma unroll 2
         for (int k = 0; k < p.K; ++k) {
-          const float* pk4 = cb + k * V;
           const float pn = norms[k];
-          float acc0[kRPL], acc1[kRPL];
+          uint64_t acc0[kRPL], acc1[kRPL];
 #pragma unroll
           for (int r = 0; r < kRPL; ++r) {
-            acc0[r] = pn;
-            acc1[r] = 0.0f;
+            acc0[r] = pack_f2(pn, 0.0f);
+            acc1[r] = 0ull;
           }
 #pragma unroll
           for (int j = 0; j < NJ; ++j) {
-            const float4 q = *reinterpret_cast<const float4*>(pk4 + 4 * j);
+            uint64_t q01, q23;
+            asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];"
+                         : "=l"(q01), "=l"(q23)
+                         : "r"(cb_s + (uint32_t)((k * V + 4 * j) * 4)));
 #pragma unroll
             for (int r = 0; r < kRPL; ++r) {
-              float& acc = (j & 1) ? acc1[r] : acc0[r];
-              acc = fmaf(a[r][4 * j + 0], q.x, acc);
-              acc = fmaf(a[r][4 * j + 1], q.y, acc);
-              acc = fmaf(a[r][4 * j + 2], q.z, acc);
-              acc = fmaf(a[r][4 * j + 3], q.w, acc);
+              acc0[r] = ffma2(a2[r][2 * j + 0], q01, acc0[r]);
+              acc1[r] = ffma2(a2[r][2 * j + 1], q23, acc1[r]);
             }
           }
 #pragma unroll
           for (int r = 0; r < kRPL; ++r) {
-            const float d = acc0[r] + acc1[r];
+            float lo, hi;
+            unpack_f2(fadd2(acc0[r], acc1[r]), lo, hi);
+            const float d = lo + hi;
             second[r] = fminf(second[r], fmaxf(best[r], d));
             bi[r] = (d < best[r]) ? k : bi[r];
             best[r] = fminf(best[r], d);
@@ -275,13 +301,14 @@ __global__ void __launch_bounds__(kEncThreads, 1)
           const float tau = tau_c * (asq[r] + pmax);
           if (!(second[r] - best[r] > tau)) {
             // near tie (or NaN): exact f64 decision from the staged tile
-            const float* rowp = reinterpret_cast<const float*>(st + r * kBoxBytes + rr * 128);
+            const int q_ = rr + r * kRowsPerPass;
+          const float* rowp = reinterpret_cast<const float*>(st + (q_ >> 8) * kBoxBytes + (q_ & 255) * 128);
             auto get_a = [&](int j) {
               const int q = sb * NJ + (j >> 2);
               return rowp[((q ^ sw) << 2) + (j & 3)];
             };
             bi[r] = exact_argmin(get_a, cb, p.K, V);
-            const int64_t row = tile * kTileRows + r * kBoxRows + rr;
+            const int64_t row = tile * kTileRows + r * kRowsPerPass + rr;
             if (p.near_tie && row < p.n) atomicAdd(p.near_tie, 1);
           }
           // shift the code into the 128-bit per-row register
@@ -324,7 +351,7 @@ __global__ void __launch_bounds__(kEncThreads, 1)
     const int64_t off = (int64_t)c_begin * bits / 8;
 #pragma unroll
     for (int r = 0; r < kRPL; ++r) {
-      const int64_t row = tile * kTileRows + r * kBoxRows + rr;
+      const int64_t row = tile * kTileRows + r * kRowsPerPass + rr;
       if (row < p.n)
         store_code_group(p.codes + row * p.code_stride + off, pk[r][0], pk[r][1], pk[r][2], pk[r][3],
                          nbytes);
@@ -492,7 +519,7 @@ static int launch_tma(const float* a, int64_t n, int d, const float* prep, int C
   const int S = prep_stride(K, V);
   constexpr int NB = 32 / V;
   const int book_bytes = NB * S * 4;
-  const int stage_bytes = ((kRPL * kBoxBytes + book_bytes) + 1023) & ~1023;
+  const int stage_bytes = ((kTileBoxes * kBoxBytes + book_bytes) + 1023) & ~1023;
   const size_t budget = max_smem_optin();
   int stages = (int)((budget - 1024 - 256) / stage_bytes);
   if (stages > 4) stages = 4;
@@ -512,6 +539,12 @@ static int launch_tma(const float* a, int64_t n, int d, const float* prep, int C
   p.near_tie = near_tie;
   p.stages = stages;
   p.stage_bytes = stage_bytes;
+  {
+    const char* e = getenv("LUTGPU_ENC_DEBUG");
+    p.debug = e ? atoi(e) : 0;
+    const char* st = getenv("LUTGPU_ENC_STAGES");
+    if (st && atoi(st) >= 2 && atoi(st) <= stages) p.stages = stages = atoi(st);
+  }
   p.ntiles = (n + kTileRows - 1) / kTileRows;
   const int nsm = num_sms();
   // group = flush granularity: 16 B of codes per row, shrunk until the grid fills the chip
