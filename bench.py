@@ -307,8 +307,18 @@ def main():
         dom, dom_ms, dom_bytes = "encode", enc_ms, encode_bytes
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     layer_hbm = 4 * n * d + s * c * k * m + 4 * c * k * v + 4 * n * m
+    traffic = None  # DRAM bytes per launch of the dominant kernel, from the committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        tc = tr["config"]
+        if (tc["d"], tc["m"], tc["v"], tc["k"], tc["table"]) == (d, m, v, k, args.table) and tensor:
+            traffic = tr[f"{dom}_dram_bytes"] / tr["rows"] * n
+    except (OSError, KeyError, ValueError):
+        pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "kernel": dom, "peak_kind": peak_kind,
+                "frac": achieved / hbm_peak, "traffic": traffic, "kernel": dom, "peak_kind": peak_kind,
+                "algorithmic_bytes": dom_bytes,
                 "kernel_ms": {"encode": enc_ms, "gather": gat_ms},
                 "smem_lookup": {"bytes": lookups * s, "achieved_TBps": lookups * s / (gat_ms / 1e3) / 1e12,
                                 "peak_TBps": smem_peak / 1e12,
