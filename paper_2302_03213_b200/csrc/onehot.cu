@@ -61,6 +61,8 @@ struct OneHotParams {
   int32_t* out_i32;
   uint32_t tmem_cols;
   int a_stages;             // A ring depth (<= kMaxAStages)
+  int n_acc;                // TMEM accumulator buffers (pair kernel: 1 or 2)
+  int spin;                 // 1: latency-critical waits poll instead of sleeping
   int tma_out;              // 1: epilogue stages the tile in SMEM and TMA-stores it
   unsigned long long* trace;  // optional per-role cycle counters (LUTGPU_OH_TRACE), CTA 0 only
   int debug;                // ablation bits (LUTGPU_OH_DEBUG): 1 no epilogue math/stores, 2 no MMA,
@@ -778,6 +780,26 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   while (!mbar_try_wait_cluster(bar, parity)) {
   }
 }
+__device__ __forceinline__ bool mbar_test_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// latency-critical wait: poll (test_wait) when spin, else sleep in try_wait
+__device__ __forceinline__ void mbar_wait_crit(uint64_t* bar, uint32_t parity, int spin) {
+  if (spin) {
+    while (!mbar_test_cluster(bar, parity)) {
+    }
+  } else {
+    mbar_wait_cluster(bar, parity);
+  }
+}
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -898,7 +920,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       mbar_init(&acc_empty[i], 9);  // 8 leader epilogue warps + 1 arrive for the peer's 8
     }
     for (int i = 0; i < p.a_stages; ++i) {
-      mbar_init(&a_full[i], 5);     // 4 leader generator warps + 1 arrive for the peer's 4
+      // leader: its 4 generator warps + 1 forward from the peer's signaler;
+      // peer: its 4 generator warps (collected locally, then forwarded)
+      mbar_init(&a_full[i], leader ? 5 : 4);
       mbar_init(&a_empty[i], 1);
     }
     fence_mbar_init();
@@ -914,7 +938,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
   if (tmem_base != 0) __trap();  // 512-column allocation must start at column 0
-  const uint32_t a_col0 = 2 * NN;  // accumulators: [0, 2*NN); A ring after
+  const uint32_t a_col0 = p.n_acc * NN;  // accumulators: [0, n_acc*NN); A ring after
 
   UnitWalk walk;
   walk.init(p, (int)(blockIdx.x >> 1), (int)(gridDim.x >> 1));
@@ -965,6 +989,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         }
       }
     }
+  } else if (warp == 1 && !leader) {
+    // ------------------------------------------------ peer signaler
+    // Forwards each ring stage the peer's generators completed to the leader's
+    // a_full (one remote release.cluster arrive per stage, off the generators'
+    // critical path).
+    uint32_t as = 0, aph = 0;
+    int ntile;
+    int64_t rt;
+    while (walk.next(ntile, rt)) {
+      for (int st = 0; st < nst; ++st) {
+        mbar_wait_crit(&a_full[as], aph, p.spin);
+        tc_fence_after();
+        tc_fence_before();
+        if (lane == 0) mbar_arrive_cluster(a_full_l + as * 8);
+        __syncwarp();
+        if (++as == nas) {
+          as = 0;
+          aph ^= 1;
+        }
+      }
+    }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (leader only)
     if (leader) {
@@ -1005,7 +1050,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int st = 0; st < nst; ++st) {
           {
             OH_T0(t0);
-            mbar_wait_cluster(&a_full[as], aph);
+            mbar_wait_crit(&a_full[as], aph, p.spin);
             OH_ACC(2, t0);
           }
           tc_fence_after();
@@ -1021,7 +1066,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         OH_ACC(3, t_unit);
         commit_elect(&acc_full[acc], true);
         if (!has_next || nt_next != ntile) commit_elect(b_empty, true);
-        if (++acc == 2) {
+        if (++acc == p.n_acc) {
           acc = 0;
           accphase ^= 1;
         }
@@ -1073,14 +1118,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           atomicAdd(p.trace + 7 + tslot, (unsigned long long)(t3 - t2));
         }
         tc_fence_before();
-        if (leader) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&a_full[as]);
-        } else {
-          // the peer's 4 warps of this parity meet locally; one remote arrive
-          named_barrier_sync(2 + par, 128);
-          if (sub == 0 && lane == 0) mbar_arrive_cluster(a_full_l + as * 8);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[as]);  // local; the peer's signaler forwards it
         cur = nxt;
         as += 2;
         if (as >= nas) {
@@ -1247,7 +1286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         }
         }  // !(debug & 1)
       }
-      if (++acc == 2) {
+      if (++acc == p.n_acc) {
         acc = 0;
         accphase ^= 1;
       }
@@ -1508,11 +1547,19 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
     p.ntiles = g.ntiles / 2;
     p.MT = NN / digits;
     p.nrt = (n + 2 * kRowsPerTile - 1) / (2 * kRowsPerTile);
-    p.a_stages = (512 - 2 * NN) / 64;
+    p.n_acc = 2;
+    p.spin = 0;
+    {
+      const char* e1 = getenv("LUTGPU_OH_ACC1");
+      if (e1 && e1[0] == '1') p.n_acc = 1;
+      const char* e2 = getenv("LUTGPU_OH_SPIN");
+      if (e2 && e2[0] == '1') p.spin = 1;
+    }
+    p.a_stages = (512 - p.n_acc * NN) / 64;
     if (p.a_stages > kMaxAStages) p.a_stages = kMaxAStages;
     if (p.a_stages < 2) return fail(LUT_ERR_CONFIG, "one-hot gather: TMEM budget exceeded");
     uint32_t alloc = 32;
-    while (alloc < (uint32_t)(2 * NN + p.a_stages * 64)) alloc <<= 1;
+    while (alloc < (uint32_t)(p.n_acc * NN + p.a_stages * 64)) alloc <<= 1;
     p.tmem_cols = alloc;
     const int nsm = num_sms();
     const int64_t units = (int64_t)p.ntiles * p.nrt;
