@@ -105,6 +105,16 @@ LUT_API int lut_encode_conv_f32(const float* x, int32_t batch, int32_t cin, int3
                         uint8_t* codes, int32_t code_bits, int32_t* near_tie_count,
                         lut_stream_t stream);
 
+/*
+ * Hash encode (hashing.encode_hash, hashing.py:171-196): one depth-L tree per
+ * codebook, level-major thresholds, left on <=.  dims (c, L) int32 indices
+ * into the sub-vector (< v), thresholds (c, 2^L - 1) f32, leaves (c, 2^L) u8.
+ * u8 codes with row stride code_stride (0 = c).  1 <= L <= 16.
+ */
+LUT_API int lut_encode_hash(const float* a, int64_t n, int32_t d, const int32_t* dims, const float* thresholds,
+                            const uint8_t* leaves, int32_t c, int32_t levels, int32_t v, uint8_t* codes,
+                            int64_t code_stride, lut_stream_t stream);
+
 /* Explicit im2col (tensor.py:36-79): cols (batch*ho*wo, cin*kh*kw). */
 LUT_API int lut_im2col_f32(const float* x, int32_t batch, int32_t cin, int32_t h, int32_t w,
                    int32_t kh, int32_t kw, int32_t stride, int32_t pad, float* cols,

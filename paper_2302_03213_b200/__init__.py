@@ -22,6 +22,7 @@ from .kernels import (
     EncodeStats,
     KernelPlan,
     centroid_search_fast,
+    encode_hash,
     flop_counter,
     lut_gather_accumulate,
     lut_gather_f32,

@@ -47,6 +47,7 @@ SIGNATURES = {
     "lut_encode_f32": (C.c_int, [P, I64, I32, P, I32, I32, I32, P, I32, I64, P, P]),
     "lut_encode_conv_f32": (C.c_int, [P, I32, I32, I32, I32, I32, I32, I32, I32, P, I32, I32, I32, P, I32, P, P]),
     "lut_im2col_f32": (C.c_int, [P, I32, I32, I32, I32, I32, I32, I32, I32, P, P]),
+    "lut_encode_hash": (C.c_int, [P, I64, I32, P, P, P, I32, I32, I32, P, I64, P]),
     "lut_gather_f32": (C.c_int, [P, I32, I64, I32, I32, I32, P, P, I32, P, I64, P, P]),
     "lut_gather_i8": (C.c_int, [P, I32, I64, I32, I32, I32, P, P, I32, P, I32, P, P, I64, P, P]),
     "lut_build_table_f32": (C.c_int, [P, I32, P, I32, I32, I32, P, P]),

@@ -26,6 +26,8 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
 int encode_conv(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad,
                 const float* prep, int C, int K, int V, uint8_t* codes, int code_bits, int* near_tie,
                 cudaStream_t stream);
+int encode_hash(const float* a, int64_t n, int d, const int* dims, const float* thr, const uint8_t* leaves, int C,
+                int L, int V, uint8_t* codes, int64_t code_stride, cudaStream_t stream);
 int im2col(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad, float* cols,
            cudaStream_t stream);
 int gather_f32(const uint8_t* codes, int code_bits, int64_t n, int C, int K, int M, const float* table,
@@ -221,6 +223,18 @@ int lut_encode_conv_f32(const float* x, int32_t batch, int32_t cin, int32_t h, i
   if (batch > 0 && (!x || !books_prep || !codes)) return fail(LUT_ERR_CONFIG, "null pointer");
   return encode_conv(x, batch, cin, h, w, kh, kw, stride, pad, static_cast<const float*>(books_prep), c, k, v,
                      codes, code_bits, near_tie_count, (cudaStream_t)stream);
+}
+
+int lut_encode_hash(const float* a, int64_t n, int32_t d, const int32_t* dims, const float* thresholds,
+                    const uint8_t* leaves, int32_t c, int32_t levels, int32_t v, uint8_t* codes, int64_t code_stride,
+                    lut_stream_t stream) {
+  if (n < 0 || c < 0 || v < 1) return fail(LUT_ERR_CONFIG, "bad hash-encode geometry");
+  if (levels < 1 || levels > 16) return fail(LUT_ERR_CONFIG, "tree depth must be in [1, 16]");
+  if ((int64_t)c * v != d) return fail(LUT_ERR_CONFIG, "input cols not divisible into the trees");
+  if (code_stride != 0 && code_stride < c) return fail(LUT_ERR_CONFIG, "code_stride smaller than a code row");
+  if (n > 0 && c > 0 && (!a || !dims || !thresholds || !leaves || !codes)) return fail(LUT_ERR_CONFIG, "null pointer");
+  return encode_hash(a, n, d, dims, thresholds, leaves, c, levels, v, codes, code_stride ? code_stride : c,
+                     (cudaStream_t)stream);
 }
 
 int lut_im2col_f32(const float* x, int32_t batch, int32_t cin, int32_t h, int32_t w, int32_t kh, int32_t kw,

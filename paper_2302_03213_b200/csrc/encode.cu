@@ -464,6 +464,39 @@ __global__ void __launch_bounds__(256) encode_rows_kernel(Rows rows, int64_t n, 
   if (code_bits == 4) codes[row * code_stride + c0 / 2] = (uint8_t)packed;
 }
 
+// ---------------------------------------------------------------- hash encode
+// Depth-L tree traversal per (row, codebook) — hashing.encode_hash
+// (lutkit/hashing.py:171-196): at level l go right iff value[dims[l]] > thr
+// (left on <=), thresholds level-major, emit the reached leaf's index.
+// L compares and no multiplications per sub-vector.
+
+__global__ void encode_hash_kernel(const float* __restrict__ a, int64_t n, int d, const int* __restrict__ dims,
+                                   const float* __restrict__ thr, const uint8_t* __restrict__ leaves, int C, int L,
+                                   int V, uint8_t* __restrict__ codes, int64_t code_stride) {
+  const int c = blockIdx.y;
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  const float* sub = a + row * d + (int64_t)c * V;
+  const int* dm = dims + c * L;
+  const float* th = thr + (int64_t)c * ((1 << L) - 1);
+  int node = 0, off = 0;
+  for (int l = 0; l < L; ++l) {
+    const float x = __ldg(sub + __ldg(dm + l));
+    node = 2 * node + (x > __ldg(th + off + node) ? 1 : 0);
+    off += 1 << l;
+  }
+  codes[row * code_stride + c] = __ldg(leaves + (int64_t)c * (1 << L) + node);
+}
+
+int encode_hash(const float* a, int64_t n, int d, const int* dims, const float* thr, const uint8_t* leaves, int C,
+                int L, int V, uint8_t* codes, int64_t code_stride, cudaStream_t stream) {
+  if (n == 0 || C == 0) return LUT_OK;
+  dim3 grid((unsigned)((n + 255) / 256), (unsigned)C);
+  encode_hash_kernel<<<grid, 256, 0, stream>>>(a, n, d, dims, thr, leaves, C, L, V, codes, code_stride);
+  LUT_CHECK_LAUNCH("encode_hash_kernel");
+  return LUT_OK;
+}
+
 // ---------------------------------------------------------------- im2col
 
 __global__ void im2col_kernel(ConvRows rows, int64_t n, int d, float* __restrict__ cols) {

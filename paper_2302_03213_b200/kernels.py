@@ -149,6 +149,54 @@ def centroid_search_fast(a, books, plan: KernelPlan = KernelPlan(), return_near_
     return (out, ties) if return_near_ties else out
 
 
+def _tree_parts(t):
+    if isinstance(t, (tuple, list)):
+        return t[0], t[1], t[2]
+    return t.dims, t.thresholds, t.leaves
+
+
+def hash_trees_device(trees, dev):
+    """Stack per-codebook trees (hashing.HashTree or (dims, thr, leaves)) into
+    device arrays; every tree must have the same depth."""
+    if not trees:
+        raise ShapeError("need at least one tree")
+    parts = [_tree_parts(t) for t in trees]
+    levels = {len(np.asarray(d)) for d, _, _ in parts}
+    if len(levels) != 1:
+        raise ConfigError("all hash trees of a layer must have the same depth")
+    L = levels.pop()
+    if not 1 <= L <= 16:
+        raise ConfigError(f"tree depth {L} outside [1, 16]")
+    dims = np.stack([np.asarray(d, np.int64) for d, _, _ in parts]).astype(np.int32)
+    thr = np.stack([np.asarray(t, np.float32) for _, t, _ in parts])
+    leaves = np.stack([np.asarray(lv, np.uint8) for _, _, lv in parts])
+    if thr.shape[1] != (1 << L) - 1 or leaves.shape[1] != (1 << L):
+        raise ShapeError("tree arrays inconsistent with their depth")
+    return (D.to_device(dims, np.int32, dev), D.to_device(thr, np.float32, dev), D.to_device(leaves, np.uint8, dev), L)
+
+
+def encode_hash(a, trees, code_stride: int = 0):
+    """Tree-traversal encoding, (N, C) u8 (hashing.py:171-196) on the GPU."""
+    n, d = _matrix_shape(a, "a")
+    if not trees:
+        raise ShapeError("need at least one tree")
+    c = len(trees)
+    if d % c != 0:
+        raise ShapeError(f"input cols {d} not divisible by {c} trees")
+    v = d // c
+    kind = D.kind_of(a)
+    dev = D.require_cuda()
+    dims, thr, leaves, L = hash_trees_device(trees, dev)
+    if int(dims.max()) >= v or int(dims.min()) < 0:
+        raise ShapeError("tree split dimension outside the sub-vector")
+    a_dev = D.to_device(a, np.float32, dev)
+    width = code_stride or c
+    codes = torch.empty((n, width), dtype=torch.uint8, device=dev)
+    check(load().lut_encode_hash(D.ptr(a_dev), n, d, D.ptr(dims), D.ptr(thr), D.ptr(leaves), c, L, v, D.ptr(codes),
+                                 width, D.stream_ptr()), "encode_hash")
+    return D.from_device(codes if width == c else codes[:, :c], kind)
+
+
 # ------------------------------------------------------------------ gather
 
 

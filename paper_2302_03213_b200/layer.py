@@ -252,7 +252,19 @@ class LutLayer:
         return D.from_device(res, kind)
 
     def infer_hash(self, a, integer: bool):
-        raise ConfigError("hash encoder is not available on the GPU path in this build")
+        """encoder="hash": tree-traversal codes, then the same lookup machinery
+        (kernels.py:159-164 — swapping the encoder only changes the indices)."""
+        from .kernels import _gather_f32, _gather_i8_f32, encode_hash
+
+        kind = D.kind_of(a)
+        codes = encode_hash(D.to_device(a, F32, self.device), self.trees)
+        act = ACTS[self.act]
+        if integer:
+            out = _gather_i8_f32(codes, self.qtable.q, self.qtable.scales_tensor(self.device), self.qtable.scale_mtile,
+                                 self.bias, act, self.c, self.k, self.m)
+        else:
+            out = _gather_f32(codes, self.table, self.bias, act, self.c, self.k, self.m)
+        return D.from_device(out, kind)
 
 
 _FOREIGN: dict[int, tuple] = {}

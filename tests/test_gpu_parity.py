@@ -348,3 +348,19 @@ def test_tc_matches_cuda_core(L, shape):
     ft = L.lut_layer_infer(a, lt, integer=False)
     fc = L.lut_layer_infer(a, lc, integer=False)
     torch.testing.assert_close(ft, fc, rtol=1e-5, atol=1e-5)
+
+
+def test_hash_encoder(L, golden):
+    """encode_hash (hashing.py:171-196) on the GPU == reference codes; the hash
+    encoder swaps only the indices (test_kernels.py:201-213)."""
+    a, trees = G.hash_inputs(golden)
+    np.testing.assert_array_equal(L.encode_hash(a, trees), golden.arrays["hash_codes"])
+    case = golden.cases("hash")
+    rng = O.make_rng(91)
+    w = rng.standard_normal((case["c"] * case["v"], 6)).astype(F32)
+    books = rng.standard_normal((case["c"], case["k"], case["v"])).astype(F32)
+    layer = L.LutLayer(cfg=L.PqConfig(v=case["v"], k=case["k"]), books=books, weight=w, bias=np.zeros(6, F32),
+                       trees=trees)
+    got = L.lut_layer_infer(a, layer, integer=False, encoder="hash")
+    want = O.lut_matmul_ref(golden.arrays["hash_codes"], O.build_table(w, books))
+    np.testing.assert_array_equal(got, want)
