@@ -33,6 +33,7 @@ from .quant import QMAX, LookupTableI8, dequantize, quantize_table
 from .pq import PqConfig, build_table, encode_hard, lut_matmul_ref, pq_amm, validate_codebooks
 from .tensor import as_matrix, im2col
 from .layer import LutLayer, as_device_layer
-from .nn import LutConv, LutConv2d, LutDense, LutLinear, predict_fast
+from .nn import Conv, Dense, LutConv, LutConv2d, LutDense, LutLinear, Model, Relu, predict_fast
+from .container import load_model, model_bytes, model_from_bytes, save_model
 
 __version__ = "0.1.0"

@@ -131,6 +131,7 @@ class LutLayer:
         self.qtable = quantize_table(self.table, self.scale_mtile) if self.qat else None
         self._desc_cache = {}
         self._images = {}
+        self.__dict__.pop("_act_twins", None)
 
     def forward_table(self):
         """Table the training forward reads: dequantized under QAT (softpq.py:134-140)."""
@@ -147,6 +148,24 @@ class LutLayer:
         self.qtable = quantize_table(self.table, self.scale_mtile)
         self._desc_cache = {}
         self._images.pop(1, None)
+        self.__dict__.pop("_act_twins", None)
+
+    def with_act(self, act) -> "LutLayer":
+        """The same device tensors with a different fused epilogue activation
+        (a LUT layer followed by Relu runs as one epilogue, model.py:27-35)."""
+        if act == self.act:
+            return self
+        cache = self.__dict__.setdefault("_act_twins", {})
+        twin = cache.get(act)
+        if twin is None:
+            if act not in ACTS:
+                raise ConfigError(f"unknown activation {act!r}")
+            twin = object.__new__(LutLayer)
+            twin.__dict__.update({k: v for k, v in self.__dict__.items() if k != "_act_twins"})
+            twin.act = act
+            twin._desc_cache = {}
+            cache[act] = twin
+        return twin
 
     # ---------------------------------------------------------------- ABI
     def uses_tensor_cores(self, integer: bool) -> bool:

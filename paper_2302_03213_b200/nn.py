@@ -114,25 +114,132 @@ class LutConv2d(torch.nn.Module):
         return conv_forward(x, self.lut, self.in_channels, self.kernel, self.stride, self.pad, self.integer)
 
 
+class Relu:
+    """max(x, 0) (model.py:27-35); after a LUT layer it is fused into that
+    layer's gather epilogue by predict_fast."""
+
+    def forward(self, x, train: bool = False):
+        if isinstance(x, torch.Tensor):
+            return torch.clamp_min(x, 0.0), None
+        return np.maximum(x, 0.0), None
+
+
+class Dense:
+    """y = x @ W + b on the GPU (model.py:38-72).  Not the LUT path: a plain
+    cuBLAS fp32 GEMM (TF32 off) for the layers a LUT model keeps dense."""
+
+    def __init__(self, weight, bias, device=None):
+        dev = torch.device(device) if device is not None else D.require_cuda()
+        self.weight = D.to_device(weight, F32, dev)
+        self.bias = D.to_device(bias, F32, dev)
+        if self.weight.dim() != 2 or self.bias.shape != (self.weight.shape[1],):
+            raise ShapeError(f"dense weight {tuple(self.weight.shape)} / bias {tuple(self.bias.shape)} mismatch")
+
+    def core_shape(self):
+        return tuple(self.weight.shape)
+
+    def forward(self, x, train: bool = False):
+        kind = D.kind_of(x)
+        t = D.to_device(x, F32, self.weight.device)
+        if t.dim() > 2:
+            t = t.reshape(t.shape[0], -1)
+        if t.shape[1] != self.weight.shape[0]:
+            raise ShapeError(f"dense layer got {t.shape[1]} features, expected {self.weight.shape[0]}")
+        return D.from_device(_matmul_f32(t, self.weight) + self.bias, kind), None
+
+
+class Conv(Dense):
+    """im2col (lut_im2col_f32) + fp32 GEMM + NCHW raise (model.py:75-133)."""
+
+    def __init__(self, in_channels: int, kernel: int, stride: int, pad: int, weight, bias, device=None):
+        super().__init__(weight, bias, device)
+        self.in_channels, self.kernel, self.stride, self.pad = in_channels, kernel, stride, pad
+        if self.weight.shape[0] != in_channels * kernel * kernel:
+            raise ShapeError(f"conv weight rows {self.weight.shape[0]} != {in_channels}*{kernel}*{kernel}")
+
+    def forward(self, x, train: bool = False):
+        from .tensor import im2col
+
+        shp = D.shape_of(x)
+        if len(shp) != 4 or shp[1] != self.in_channels:
+            raise ShapeError(f"conv expected NCHW with {self.in_channels} channels, got {shp}")
+        kind = D.kind_of(x)
+        ho, wo = conv_out_hw(shp[2], shp[3], self.kernel, self.kernel, self.stride, self.pad)
+        cols = im2col(D.to_device(x, F32, self.weight.device), self.kernel, self.kernel, self.stride, self.pad)
+        y = _matmul_f32(cols, self.weight) + self.bias
+        out = y.reshape(shp[0], ho, wo, -1).permute(0, 3, 1, 2).contiguous()
+        return D.from_device(out, kind), None
+
+
+def _matmul_f32(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        return a @ b
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+class Model:
+    """Ordered layer stack (model.py:224-244); `predict_logits` runs the
+    fast path."""
+
+    def __init__(self, layers: list):
+        self.layers = layers
+
+    def predict_logits(self, x, encoder: str = "dist", integer=None):
+        return predict_fast(self, x, encoder=encoder, integer=integer)
+
+
+def _is_lut(layer, cls) -> bool:
+    return getattr(layer, "lut", None) is not None and (isinstance(layer, cls) or type(layer).__name__ == cls.__name__)
+
+
+def _is_relu(layer) -> bool:
+    return isinstance(layer, Relu) or type(layer).__name__ == "Relu"
+
+
 def predict_fast(model, x, plan: KernelPlan = KernelPlan(), encoder: str = "dist", integer=None):
     """Inference through the GPU kernels; non-LUT layers run their own
     forward (pipeline.py:206-225).  Accepts a reference-style model (object
     with `.layers`) or any iterable of layers; reference LutDense/LutConv
-    instances are recognised by their attributes."""
+    instances are recognised by their attributes.  A Relu right after a LUT
+    layer is fused into that layer's gather epilogue (same values: the
+    reference applies max(y, 0) to the layer's f32 output)."""
     layers = model.layers if hasattr(model, "layers") else list(model)
-    for layer in layers:
-        lut = getattr(layer, "lut", None)
-        name = type(layer).__name__
-        if lut is not None and (isinstance(layer, LutConv) or name == "LutConv"):
-            x = conv_forward(x, as_device_layer(lut), layer.in_channels, layer.kernel, layer.stride, layer.pad,
-                             integer)
-        elif lut is not None and (isinstance(layer, LutDense) or name == "LutDense"):
-            shp = D.shape_of(x)
-            if len(shp) > 2:
-                x = x.reshape(shp[0], -1)
-            x = lut_layer_infer(x, lut, plan, integer=integer, encoder=encoder)
+    kind = D.kind_of(x)
+    i = 0
+    while i < len(layers):
+        layer = layers[i]
+        conv, dense = _is_lut(layer, LutConv), _is_lut(layer, LutDense)
+        if conv or dense:
+            lut = as_device_layer(layer.lut)
+            if i + 1 < len(layers) and _is_relu(layers[i + 1]) and lut.act in (None, "none"):
+                lut = lut.with_act("relu")
+                i += 1
+            if conv:
+                if encoder != "dist":
+                    from .tensor import im2col
+
+                    shp = D.shape_of(x)
+                    ho, wo = conv_out_hw(shp[2], shp[3], layer.kernel, layer.kernel, layer.stride, layer.pad)
+                    cols = im2col(D.to_device(x, F32, lut.device), layer.kernel, layer.kernel, layer.stride,
+                                  layer.pad)
+                    y = lut_layer_infer(cols, lut, plan, integer=integer, encoder=encoder)
+                    x = y.reshape(shp[0], ho, wo, -1).permute(0, 3, 1, 2).contiguous()
+                else:
+                    x = conv_forward(D.to_device(x, F32, lut.device), lut, layer.in_channels, layer.kernel,
+                                     layer.stride, layer.pad, integer)
+            else:
+                x = D.to_device(x, F32, lut.device)
+                if x.dim() > 2:
+                    x = x.reshape(x.shape[0], -1)
+                x = lut_layer_infer(x, lut, plan, integer=integer, encoder=encoder)
         elif isinstance(layer, torch.nn.Module):
             x = layer(x)
-        else:
+        elif isinstance(layer, (Dense, Relu)):
             x, _ = layer.forward(x, train=False)
-    return x
+        else:  # a foreign (reference numpy) layer: hand it host data
+            x, _ = layer.forward(x.cpu().numpy() if isinstance(x, torch.Tensor) else x, train=False)
+        i += 1
+    return D.from_device(x, kind) if isinstance(x, torch.Tensor) else x

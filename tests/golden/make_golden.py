@@ -22,6 +22,8 @@ Case families mirror the reference's own tests for the path:
   cfg5s      configs[4] encode geometry (D=4096, V=32, K=16 and 64) on a 2048-row subsample
   conv       configs[2] geometry on a batch-2 sample (16ch 8x8, V=9, K=16)
   hash       hashing.py:171-196 trees built by the reference on a seeded sample
+  lutn_*     container.py:1-23 models written by the reference (bytes stored) and
+             its predict_fast outputs on the loaded model (pipeline.py:206-225)
 """
 
 from __future__ import annotations
@@ -272,10 +274,64 @@ def main() -> None:
     arrays["hash_codes"] = hashing.encode_hash(samples[:64], trees)
     meta["cases"]["hash"] = {"seed": 77, "c": c, "v": v, "k": k, "levels": lv, "rows": 64}
 
+    _lutn_cases(arrays, meta)
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(meta, f, indent=1)
     print("wrote", len(arrays), "arrays")
+
+
+def _lut(rng, c, k, v, m, qat, bias=True, tree_levels=0, samples=None):
+    books = rng.standard_normal((c, k, v)).astype(F32)
+    weight = rng.standard_normal((c * v, m)).astype(F32)
+    b = rng.standard_normal(m).astype(F32) if bias else np.zeros(m, F32)
+    lut = LutLayer(cfg=pq.PqConfig(v=v, k=k), books=books, weight=weight, bias=b, qat=qat)
+    if tree_levels:
+        lut.trees = [hashing.build_hash_tree(samples[:, i * v:(i + 1) * v], books[i], tree_levels) for i in range(c)]
+    return lut
+
+
+def _lutn_cases(arrays, meta):
+    """Containers written by the reference + predict_fast of the loaded model."""
+    from lutkit import container, pipeline
+    from lutkit.model import Conv, Dense, LutConv, LutDense, Model, Relu
+
+    # A: LutDense(f32, bias, trees) -> relu -> LutDense(i8, bias, trees) -> relu -> Dense
+    rng = make_rng(501)
+    x = rng.standard_normal((96, 16)).astype(F32)
+    l1 = _lut(rng, 4, 8, 4, 12, qat=False, tree_levels=3, samples=x)
+    h = np.maximum(kernels.lut_layer_infer(x, l1), 0)
+    l2 = _lut(rng, 3, 16, 4, 7, qat=True, tree_levels=4, samples=np.pad(h, ((0, 0), (0, 0))))
+    head = Dense(7, 3, rng)
+    head.bias = rng.standard_normal(3).astype(F32)
+    model = Model([LutDense(l1), Relu(), LutDense(l2), Relu(), head])
+    raw = container.model_bytes(model)
+    loaded = container.model_from_bytes(raw)
+    arrays["lutn_a_bytes"] = np.frombuffer(raw, np.uint8)
+    arrays["lutn_a_x"] = x
+    arrays["lutn_a_dist"] = pipeline.predict_fast(loaded, x)
+    arrays["lutn_a_f32"] = pipeline.predict_fast(loaded, x, integer=False)
+    arrays["lutn_a_hash"] = pipeline.predict_fast(loaded, x, encoder="hash")
+    arrays["lutn_a_hidden"] = pipeline.predict_fast(Model(loaded.layers[:4]), x)
+
+    # B: LutConv(i8) -> relu -> Conv -> relu -> Dense(flatten)
+    rng = make_rng(502)
+    x = rng.standard_normal((2, 3, 8, 8)).astype(F32)
+    lc = _lut(rng, 3, 16, 9, 8, qat=True)
+    conv = Conv(8, 4, kernel=3, stride=2, pad=1, rng=rng)
+    conv.bias = rng.standard_normal(4).astype(F32)
+    head = Dense(4 * 4 * 4, 10, rng)
+    model = Model([LutConv(3, 3, 1, 1, lc), Relu(), conv, Relu(), head])
+    raw = container.model_bytes(model)
+    loaded = container.model_from_bytes(raw)
+    arrays["lutn_b_bytes"] = np.frombuffer(raw, np.uint8)
+    arrays["lutn_b_x"] = x
+    arrays["lutn_b_dist"] = pipeline.predict_fast(loaded, x)
+    arrays["lutn_b_f32"] = pipeline.predict_fast(loaded, x, integer=False)
+    arrays["lutn_b_conv"] = pipeline.predict_fast(Model(loaded.layers[:2]), x)
+    meta["cases"]["lutn"] = {"a_seed": 501, "b_seed": 502, "a_len": int(arrays["lutn_a_bytes"].size),
+                             "b_len": int(arrays["lutn_b_bytes"].size)}
 
 
 def _gaps(a, books):
