@@ -464,6 +464,213 @@ __global__ void __launch_bounds__(256) encode_rows_kernel(Rows rows, int64_t n, 
   if (code_bits == 4) codes[row * code_stride + c0 / 2] = (uint8_t)packed;
 }
 
+// ------------------------------------------------------- conv plane path
+// A LutConv whose codebook is one input channel's kh x kw patch (V = kh*kw,
+// C = Cin: configs[2]) encodes each (image, channel) plane independently.
+// Unit = (plane group g of 8 channels, image b); units are g-major so a
+// persistent CTA keeps its centroids in registers across consecutive units.
+// The group's 8 planes (contiguous in NCHW) arrive by one cp.async.bulk into
+// a double-buffered SMEM slot while the previous unit computes; warp w owns
+// plane w: its K x V centroids live in registers as (k, k+1) pairs and every
+// distance is FFMA2.  Padding is a predicate on the SMEM read, no halo copy.
+// Codes are staged per unit and stored 8 channels (8 bytes) per pixel.
+
+constexpr int kConvWarps = 8;
+
+struct ConvPlaneParams {
+  const float* x;
+  const float* prep;
+  int S;
+  int batch, cin, h, w, stride, pad, ho, wo;
+  int ngroups;
+  int64_t nunits;
+  uint8_t* codes;
+  int64_t code_stride;
+  int* near_tie;
+  uint32_t plane_bytes;  // h*w*4
+  uint32_t slot_bytes;   // 8 planes, 128-aligned
+};
+
+template <int K, int KH>
+__global__ void __launch_bounds__(kConvWarps * 32, 1) encode_conv_plane_kernel(ConvPlaneParams p) {
+  constexpr int V = KH * KH;
+  constexpr int KP = K / 2;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  float* slot[2] = {reinterpret_cast<float*>(smem), reinterpret_cast<float*>(smem + p.slot_bytes)};
+  uint8_t* cst = smem + 2 * p.slot_bytes;  // ho*wo x 8 code bytes
+  uint64_t* bar = reinterpret_cast<uint64_t*>(cst + (((size_t)p.ho * p.wo * 8 + 15) & ~(size_t)15));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hw_out = p.ho * p.wo;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int64_t u, int s) {
+    const int g = (int)(u / p.batch), b = (int)(u - (int64_t)g * p.batch);
+    const int nplanes = min(kConvWarps, p.cin - g * kConvWarps);
+    const uint32_t bytes = (uint32_t)nplanes * p.plane_bytes;
+    mbar_arrive_expect_tx(&bar[s], bytes);
+    bulk_load(slot[s], p.x + ((int64_t)b * p.cin + (int64_t)g * kConvWarps) * p.h * p.w, bytes, &bar[s]);
+  };
+  int64_t u = blockIdx.x;
+  if (threadIdx.x == 0 && u < p.nunits) issue(u, 0);
+
+  uint64_t cp[KP][V];  // centroid pairs (k even, k odd) per coordinate
+  uint64_t np[KP];     // norm pairs
+  float pmax = 0.0f;
+  int cur_c = -1;
+  const float tau_c = tau_coef(V);
+  for (int it = 0; u < p.nunits; u += gridDim.x, ++it) {
+    const int s = it & 1;
+    const int g = (int)(u / p.batch), b = (int)(u - (int64_t)g * p.batch);
+    if (threadIdx.x == 0 && u + gridDim.x < p.nunits) {
+      fence_proxy_async_smem();
+      issue(u + gridDim.x, s ^ 1);
+    }
+    const int c = g * kConvWarps + warp;
+    if (c < p.cin && c != cur_c) {
+      const float* rec = p.prep + (size_t)c * p.S;
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) cp[k][j] = pack_f2(__ldg(rec + (2 * k) * V + j), __ldg(rec + (2 * k + 1) * V + j));
+        np[k] = pack_f2(__ldg(rec + K * V + 2 * k), __ldg(rec + K * V + 2 * k + 1));
+      }
+      pmax = __ldg(rec + K * V + K);
+      cur_c = c;
+    }
+    mbar_wait(&bar[s], (uint32_t)(it >> 1) & 1u);
+    if (c < p.cin) {
+      const float* plane = slot[s] + (size_t)warp * (p.plane_bytes / 4);
+      // two pixels per lane per pass: independent FFMA2 / argmin chains for ILP
+      constexpr int R = 2;
+      const float inv_wo = 1.0f / (float)p.wo;
+      for (int base = 0; base < hw_out; base += 32 * R) {
+        int pixr[R], y0[R], x0[R];
+        float a[R][V], asq[R];
+        uint64_t acc[R][KP];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int pix = min(base + r * 32 + lane, hw_out - 1);  // clamped lanes recompute a valid pixel
+          const int oy = __float2int_rz(((float)pix + 0.5f) * inv_wo), ox = pix - oy * p.wo;
+          pixr[r] = base + r * 32 + lane;
+          y0[r] = oy * p.stride - p.pad;
+          x0[r] = ox * p.stride - p.pad;
+          asq[r] = 0.0f;
+#pragma unroll
+          for (int dy = 0; dy < KH; ++dy) {
+#pragma unroll
+            for (int dx = 0; dx < KH; ++dx) {
+              const int iy = y0[r] + dy, ix = x0[r] + dx;
+              const bool in = (unsigned)iy < (unsigned)p.h && (unsigned)ix < (unsigned)p.w;
+              const float v = in ? plane[iy * p.w + ix] : 0.0f;
+              a[r][dy * KH + dx] = v;
+              asq[r] = fmaf(v, v, asq[r]);
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < KP; ++k) acc[r][k] = np[k];
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const float m2 = -2.0f * a[r][j];
+            const uint64_t a2 = pack_f2(m2, m2);
+#pragma unroll
+            for (int k = 0; k < KP; ++k) acc[r][k] = ffma2(a2, cp[k][j], acc[r][k]);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float best = FLT_MAX, second = FLT_MAX;
+          int bi = 0;
+#pragma unroll
+          for (int k = 0; k < KP; ++k) {
+            float d0, d1;
+            unpack_f2(acc[r][k], d0, d1);
+            second = fminf(second, fmaxf(best, d0));
+            bi = (d0 < best) ? 2 * k : bi;
+            best = fminf(best, d0);
+            second = fminf(second, fmaxf(best, d1));
+            bi = (d1 < best) ? 2 * k + 1 : bi;
+            best = fminf(best, d1);
+          }
+          if (pixr[r] < hw_out) {
+            if (!(second - best > tau_c * (asq[r] + pmax))) {
+              const int H = p.h, W = p.w, yy = y0[r], xx = x0[r];
+              auto get_a = [plane, yy, xx, H, W](int j) {
+                const int iy = yy + j / KH, ix = xx + j % KH;
+                return ((unsigned)iy < (unsigned)H && (unsigned)ix < (unsigned)W) ? plane[iy * W + ix] : 0.0f;
+              };
+              bi = exact_argmin(get_a, p.prep + (size_t)c * p.S, K, V);
+              if (p.near_tie) atomicAdd(p.near_tie, 1);
+            }
+            cst[pixr[r] * 8 + warp] = (uint8_t)bi;
+          }
+        }
+      }
+    }
+    __syncthreads();  // codes staged; slot s fully consumed
+    {
+      const int nplanes = min(kConvWarps, p.cin - g * kConvWarps);
+      uint8_t* dst0 = p.codes + ((int64_t)b * hw_out) * p.code_stride + g * kConvWarps;
+      if (nplanes == kConvWarps && (p.code_stride & 7) == 0 && (reinterpret_cast<uintptr_t>(p.codes) & 7) == 0) {
+        for (int pix = threadIdx.x; pix < hw_out; pix += blockDim.x)
+          *reinterpret_cast<uint2*>(dst0 + (int64_t)pix * p.code_stride) = *reinterpret_cast<const uint2*>(cst + pix * 8);
+      } else {
+        for (int i = threadIdx.x; i < hw_out * nplanes; i += blockDim.x) {
+          const int pix = i / nplanes, q = i - pix * nplanes;
+          dst0[(int64_t)pix * p.code_stride + q] = cst[pix * 8 + q];
+        }
+      }
+    }
+    __syncthreads();  // code staging reusable
+  }
+}
+
+template <int K, int KH>
+static int launch_conv_plane(const float* x, int batch, int cin, int h, int w, int stride, int pad, int ho, int wo,
+                             const float* prep, uint8_t* codes, int64_t code_stride, int* near_tie,
+                             cudaStream_t stream, bool* used) {
+  *used = false;
+  ConvPlaneParams p;
+  p.plane_bytes = (uint32_t)h * w * 4;
+  if ((p.plane_bytes & 15) || (reinterpret_cast<uintptr_t>(x) & 15)) return LUT_OK;
+  p.slot_bytes = (p.plane_bytes * kConvWarps + 127) & ~127u;
+  const size_t smem = 2 * (size_t)p.slot_bytes + (((size_t)ho * wo * 8 + 15) & ~(size_t)15) + 16 + 128;
+  if (smem > max_smem_optin()) return LUT_OK;
+  p.x = x;
+  p.prep = prep;
+  p.S = prep_stride(K, KH * KH);
+  p.batch = batch;
+  p.cin = cin;
+  p.h = h;
+  p.w = w;
+  p.stride = stride;
+  p.pad = pad;
+  p.ho = ho;
+  p.wo = wo;
+  p.ngroups = (cin + kConvWarps - 1) / kConvWarps;
+  p.nunits = (int64_t)p.ngroups * batch;
+  p.codes = codes;
+  p.code_stride = code_stride;
+  p.near_tie = near_tie;
+  auto kern = encode_conv_plane_kernel<K, KH>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(encode_conv_plane)");
+  const int nsm = num_sms();
+  const int grid = (int)(p.nunits < nsm ? p.nunits : nsm);
+  kern<<<grid, kConvWarps * 32, smem, stream>>>(p);
+  LUT_CHECK_LAUNCH("encode_conv_plane_kernel");
+  *used = true;
+  return LUT_OK;
+}
+
 // ---------------------------------------------------------------- hash encode
 // Depth-L tree traversal per (row, codebook) — hashing.encode_hash
 // (lutkit/hashing.py:171-196): at level l go right iff value[dims[l]] > thr
@@ -628,6 +835,19 @@ int encode_conv(const float* x, int batch, int cin, int h, int w, int kh, int kw
   if (n == 0 || C == 0) return LUT_OK;
   ConvRows rows{x, cin, h, w, kh, kw, stride, pad, ho, wo};
   const int64_t code_stride = code_bits == 4 ? (C + 1) / 2 : C;
+  const char* force = getenv("LUTGPU_CONV_GENERIC");
+  if (code_bits == 8 && kh == 3 && kw == 3 && V == 9 && C == cin && !(force && atoi(force))) {
+    bool used = false;
+    int st = LUT_OK;
+    if (K == 16)
+      st = launch_conv_plane<16, 3>(x, batch, cin, h, w, stride, pad, ho, wo, prep, codes, code_stride, near_tie,
+                                    stream, &used);
+    else if (K == 8)
+      st = launch_conv_plane<8, 3>(x, batch, cin, h, w, stride, pad, ho, wo, prep, codes, code_stride, near_tie,
+                                   stream, &used);
+    if (st != LUT_OK) return st;
+    if (used) return LUT_OK;
+  }
   return launch_rows(nullptr, &rows, n, prep, C, K, V, codes, code_bits, code_stride, near_tie, stream);
 }
 
