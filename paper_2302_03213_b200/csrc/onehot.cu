@@ -38,7 +38,7 @@ namespace lutgpu {
 constexpr int kOhThreads = 16 * 32;
 constexpr int kRowsPerTile = 128;
 constexpr int kKB = 128;       // K bytes per A stage / B block
-constexpr int kMaxAStages = 12;  // A ring depth: fills TMEM (2*NT accumulator + 32/stage)
+constexpr int kMaxAStages = 24;  // A ring depth bound (barrier arrays)
 
 struct OneHotParams {
   const uint8_t* b_image;   // [ntiles][nkb][NT][128] swizzled
@@ -65,6 +65,8 @@ struct OneHotParams {
   int spin;                 // 1: latency-critical waits poll instead of sleeping
   int tma_out;              // 1: epilogue stages the tile in SMEM and TMA-stores it
   unsigned long long* trace;  // optional per-role cycle counters (LUTGPU_OH_TRACE), CTA 0 only
+  int sparse;               // 2:4-compressed one-hot A (tcgen05.mma.sp), else dense
+  int stage_kb;             // pair kernel, sparse: 128-byte K blocks per A ring stage (1 or 2)
   int debug;                // ablation bits (LUTGPU_OH_DEBUG): 1 no epilogue math/stores, 2 no MMA,
                             // 4 no TMEM A stores, 8 MMA only (no A handshake, generators idle)
 };
@@ -264,10 +266,10 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // Code bytes of one ring stage (two 128-byte K blocks) for this row, read
 // from the 128B-swizzled code tile (16-byte chunk j of row r at
 // ((j ^ (r & 7)) << 4), 16 KB per 128-column box).
-template <int K>
+template <int K, int KB = 2>
 struct StageCodes {
   static constexpr int CPB = kKB / K;          // codebooks per K block
-  static constexpr int CPS = 2 * CPB;          // codebooks per stage
+  static constexpr int CPS = KB * CPB;         // codebooks per stage
   static constexpr int NW = (CPS + 3) / 4;     // code words per stage
   uint32_t w[NW];
   __device__ __forceinline__ void load(uint32_t row_saddr, int sw, int st) {
@@ -329,6 +331,92 @@ __device__ __forceinline__ void build_onehot(const StageCodes<K>& cd, uint32_t (
   }
 }
 
+// 2:4-compressed one-hot of a stage for tcgen05.mma.sp (kind::i8).  Logical
+// position P = cb*K + code lies in group G = P/4 with hot slot h = code&3.
+// Every group of a codebook uses the same position pair: (2,3) if code&2
+// else (0,1) (cold groups carry zeros, so their pair is free), hence the
+// compressed row holds byte 2*(code>>2) + (code&1) = 1 and zeros elsewhere,
+// and the codebook's metadata nibbles (i0 | i1<<2, little-endian per group,
+// 8 groups per 32-bit TMEM column) are all 0xE or all 0x4 (layout verified
+// against dense results by tools/sparse_probe.cu).  Four codes are
+// processed per 32-bit word with byte-parallel masks.
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t s) {  // PTX: s >= 32 gives 0
+  uint32_t r;
+  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(s));
+  return r;
+}
+
+template <int K, int KB = 2>
+__device__ __forceinline__ void build_sparse(const StageCodes<K, KB>& cd, uint32_t (&a)[16 * KB],
+                                             uint32_t (&e)[4 * KB]) {
+  constexpr int CPS = StageCodes<K, KB>::CPS;
+  if constexpr (K == 16 || K == 8) {
+#pragma unroll
+    for (int i = 0; i < CPS / 4; ++i) {
+      const uint32_t W = cd.w[i] & (0x01010101u * (K - 1));
+      const uint32_t bp8 = ((((W >> 1) & 0x06060606u) | (W & 0x01010101u)) << 3);  // 8 * compressed byte
+      const uint32_t hb = (W >> 1) & 0x01010101u;                                    // pair (2,3) flag
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t sh = __byte_perm(bp8, 0, 0x4440 + j);
+        if constexpr (K == 16) {  // 8 compressed bytes = 2 words; 4 groups = 16 metadata bits
+          a[(4 * i + j) * 2 + 0] = shl_clamp(1u, sh);
+          a[(4 * i + j) * 2 + 1] = shl_clamp(1u, sh - 32u);
+        } else {  // 4 compressed bytes = 1 word; 2 groups = 8 metadata bits
+          a[4 * i + j] = shl_clamp(1u, sh);
+        }
+      }
+      if constexpr (K == 16) {  // metadata word = 2 codebooks: nibbles 0x4 + 0xA*flag (disjoint bits)
+        e[2 * i + 0] = __byte_perm(hb, 0, 0x4140) * 0xAAAAu + 0x44444444u;
+        e[2 * i + 1] = __byte_perm(hb, 0, 0x4342) * 0xAAAAu + 0x44444444u;
+      } else {  // metadata word = 4 codebooks, one byte each
+        e[i] = hb * 0xAAu + 0x44444444u;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4 * KB; ++i) e[i] = 0x44444444u;
+#pragma unroll
+    for (int cb = 0; cb < CPS; ++cb) {
+      const uint32_t code = __byte_perm(cd.w[cb >> 2], 0, 0x4440 + (cb & 3)) & (K - 1);
+      const uint32_t bytepos = 2u * (code >> 2) + (code & 1u);  // compressed byte inside the codebook
+      const uint32_t flag = (code >> 1) & 1u;
+      if constexpr (K == 4) {  // 2 bytes = half word; 1 group = 1 nibble
+        if ((cb & 1) == 0) a[cb >> 1] = 0u;
+        a[cb >> 1] |= 1u << (16 * (cb & 1) + (bytepos << 3));
+        e[cb >> 3] ^= (flag * 0xAu) << (4 * (cb & 7));
+      } else {  // K >= 32: K/8 words and K/32 metadata words (all 0xE or all 0x4) per codebook
+        constexpr int WPC = K / 8;
+        constexpr int EPC = K / 32;
+        const uint32_t wi = bytepos >> 2, bit = 1u << ((bytepos & 3) << 3);
+#pragma unroll
+        for (int j = 0; j < WPC; ++j) a[cb * WPC + j] = (wi == (uint32_t)j) ? bit : 0u;
+#pragma unroll
+        for (int j = 0; j < EPC; ++j) e[cb * EPC + j] = flag ? 0xEEEEEEEEu : 0x44444444u;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_st64(uint32_t taddr, const uint32_t (&v)[64]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -346,6 +434,116 @@ __device__ __forceinline__ void tmem_st64(uint32_t taddr, const uint32_t (&v)[64
       : "memory");
 }
 
+// One ring stage (up to two 128-byte K blocks = 8 MMAs) issued from a single
+// asm block executed by the whole warp, predicated on elect.sync: operands stay
+// warp-uniform (no per-MMA R2UR/ELECT loop in SASS) and the 8 address offsets
+// are immediates.  acc0 = accumulate flag of the stage's first MMA.
+#define OH_MMA_G(G, AOFF, BOFF, PRED)       \
+  "add.u32 ta, %1, " #AOFF ";\n\t"        \
+  "add.u64 tb, %2, " #BOFF ";\n\t"        \
+  "@e tcgen05.mma.cta_group::" #G ".kind::i8 [%0], [ta], tb, %4, " #PRED ";\n\t"
+#define OH_MMA_H(G, AOFF, BOFF)             \
+  "add.u32 ta, %1, " #AOFF ";\n\t"        \
+  "add.u64 tb, tb2, " #BOFF ";\n\t"       \
+  "@e tcgen05.mma.cta_group::" #G ".kind::i8 [%0], [ta], tb, %4, pt2;\n\t"
+#define OH_STAGE_ASM(G)                                                                      \
+  "{\n\t.reg .pred e, p0, pt2, e2;\n\t.reg .b32 ta;\n\t.reg .b64 tb, tb2;\n\t"            \
+  "elect.sync _|e, 0xffffffff;\n\t"                                                         \
+  "setp.ne.u32 p0, %5, 0;\n\t"                                                              \
+  "setp.eq.u32 pt2, %4, %4;\n\t"                                                            \
+  OH_MMA_G(G, 0, 0, p0) OH_MMA_G(G, 8, 2, pt2) OH_MMA_G(G, 16, 4, pt2) OH_MMA_G(G, 24, 6, pt2) \
+  "setp.ne.u32 e2, %6, 0;\n\t"                                                              \
+  "and.pred e, e, e2;\n\t"                                                                  \
+  "add.u64 tb2, %2, %3;\n\t"                                                                \
+  OH_MMA_H(G, 32, 0) OH_MMA_H(G, 40, 2) OH_MMA_H(G, 48, 4) OH_MMA_H(G, 56, 6) "}"
+
+// Sparse stage: 4 tcgen05.mma.sp (K = 64 logical each): compressed A 8 TMEM
+// columns and metadata 2 columns per MMA, B advanced 64 bytes per MMA.
+#define OH_SP_G(G, AOFF, BOFF, EOFF, PRED) \
+  "add.u32 ta, %1, " #AOFF ";\n\t"       \
+  "add.u64 tb, %2, " #BOFF ";\n\t"       \
+  "add.u32 te, %7, " #EOFF ";\n\t"       \
+  "@e tcgen05.mma.sp.cta_group::" #G ".kind::i8 [%0], [ta], tb, [te], %4, " #PRED ";\n\t"
+#define OH_SP_H(G, AOFF, BOFF, EOFF)       \
+  "add.u32 ta, %1, " #AOFF ";\n\t"       \
+  "add.u64 tb, tb2, " #BOFF ";\n\t"      \
+  "add.u32 te, %7, " #EOFF ";\n\t"       \
+  "@e tcgen05.mma.sp.cta_group::" #G ".kind::i8 [%0], [ta], tb, [te], %4, pt2;\n\t"
+#define OH_SP_STAGE_ASM(G)                                                   \
+  "{\n\t.reg .pred e, p0, pt2, e2;\n\t.reg .b32 ta, te;\n\t.reg .b64 tb, tb2;\n\t" \
+  "elect.sync _|e, 0xffffffff;\n\t"                                        \
+  "setp.ne.u32 p0, %5, 0;\n\t"                                             \
+  "setp.eq.u32 pt2, %4, %4;\n\t"                                           \
+  OH_SP_G(G, 0, 0, 0, p0) OH_SP_G(G, 8, 4, 2, pt2)                          \
+  "setp.ne.u32 e2, %6, 0;\n\t"                                             \
+  "and.pred e, e, e2;\n\t"                                                 \
+  "add.u64 tb2, %2, %3;\n\t"                                               \
+  OH_SP_H(G, 16, 0, 4) OH_SP_H(G, 24, 4, 6) "}"
+
+#define OH_SP1_STAGE_ASM(G)                                                  \
+  "{\n\t.reg .pred e, p0, pt2;\n\t.reg .b32 ta, te;\n\t.reg .b64 tb;\n\t"      \
+  "elect.sync _|e, 0xffffffff;\n\t"                                        \
+  "setp.ne.u32 p0, %4, 0;\n\t"                                             \
+  "setp.eq.u32 pt2, %3, %3;\n\t"                                           \
+  "add.u32 ta, %1, 0;\n\tadd.u64 tb, %2, 0;\n\tadd.u32 te, %5, 0;\n\t"    \
+  "@e tcgen05.mma.sp.cta_group::" #G ".kind::i8 [%0], [ta], tb, [te], %3, p0;\n\t" \
+  "add.u32 ta, %1, 8;\n\tadd.u64 tb, %2, 4;\n\tadd.u32 te, %5, 2;\n\t"    \
+  "@e tcgen05.mma.sp.cta_group::" #G ".kind::i8 [%0], [ta], tb, [te], %3, pt2;\n\t}"
+
+// one-K-block sparse stage: 2 tcgen05.mma.sp
+template <int CG>
+__device__ __forceinline__ void issue_stage_sp1(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc0,
+                                                uint32_t meta) {
+  if constexpr (CG == 2) {
+    asm volatile(OH_SP1_STAGE_ASM(2)::"r"(d), "r"(a), "l"(b), "r"(idesc), "r"(acc0), "r"(meta) : "memory");
+  } else {
+    asm volatile(OH_SP1_STAGE_ASM(1)::"r"(d), "r"(a), "l"(b), "r"(idesc), "r"(acc0), "r"(meta) : "memory");
+  }
+}
+
+template <int CG>
+__device__ __forceinline__ void issue_stage_sp(uint32_t d, uint32_t a, uint64_t b, uint64_t bstep, uint32_t idesc,
+                                               uint32_t acc0, uint32_t two, uint32_t meta) {
+  if constexpr (CG == 2) {
+    asm volatile(OH_SP_STAGE_ASM(2)::"r"(d), "r"(a), "l"(b), "l"(bstep), "r"(idesc), "r"(acc0), "r"(two), "r"(meta)
+                 : "memory");
+  } else {
+    asm volatile(OH_SP_STAGE_ASM(1)::"r"(d), "r"(a), "l"(b), "l"(bstep), "r"(idesc), "r"(acc0), "r"(two), "r"(meta)
+                 : "memory");
+  }
+}
+
+// One ring stage (up to two 128-byte K blocks = 8 MMAs) issued from a single
+// asm block executed by the whole warp, predicated on elect.sync: operands stay
+// warp-uniform (no per-MMA R2UR/ELECT loop in SASS) and the 8 address offsets
+// are immediates.  acc0 = accumulate flag of the stage's first MMA; two = the
+// stage holds a second K block.
+template <int CG>
+__device__ __forceinline__ void issue_stage(uint32_t d, uint32_t a, uint64_t b, uint64_t bstep, uint32_t idesc,
+                                            uint32_t acc0, uint32_t two) {
+  if constexpr (CG == 2) {
+    asm volatile(OH_STAGE_ASM(2)::"r"(d), "r"(a), "l"(b), "l"(bstep), "r"(idesc), "r"(acc0), "r"(two) : "memory");
+  } else {
+    asm volatile(OH_STAGE_ASM(1)::"r"(d), "r"(a), "l"(b), "l"(bstep), "r"(idesc), "r"(acc0), "r"(two) : "memory");
+  }
+}
+
+// tcgen05.commit from an elected lane (whole warp executes it)
+__device__ __forceinline__ void commit_elect(uint64_t* bar, bool pair) {
+  if (pair)
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
 // cycle accounting for the LUTGPU_OH_TRACE diagnostic (CTA 0, one lane per role)
 #define OH_T0(var) long long var = (p.trace && blockIdx.x == 0) ? clock64() : 0
 #define OH_ACC(slot, var) \
@@ -358,12 +556,14 @@ constexpr int kEpiWarp0 = 12;  // warps 12..15: epilogue (pair kernel: 12..19, o
 constexpr int kPairThreads = 20 * 32;
 constexpr int kGenWarps = 8;
 constexpr int kStageCols = 64;  // TMEM columns per A stage (2 K blocks x 128 B / 4 B)
+constexpr int kSparseStageCols = 40;  // 2:4 sparse stage: 32 compressed A + 8 metadata columns
 
-template <int K, int DIGITS>
+template <int K, int DIGITS, int SP>
 __global__ void __launch_bounds__(kOhThreads, 1)
     onehot_gemm_kernel(const __grid_constant__ CUtensorMap codes_map, const __grid_constant__ CUtensorMap out_map,
                        const __grid_constant__ OneHotParams p) {
   static_assert(K >= 4, "K >= 4 on the tensor-core path");
+  constexpr int SC = SP ? kSparseStageCols : kStageCols;  // TMEM columns per A ring stage
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window (LDS, not generic LD)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -456,7 +656,8 @@ __global__ void __launch_bounds__(kOhThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    const uint32_t idesc = idesc_i8(128, p.NT);
+    const uint32_t idesc = idesc_i8(128, p.NT) | (SP ? 4u : 0u);  // bit 2: sparse A
+    const uint64_t bstep1 = (uint64_t)((p.NT * kKB) >> 4);          // descriptor step of one K block
     int cur_ntile = -1;
     uint32_t b_phase = 0;
     uint32_t as = 0, aph = 0;  // A stage / phase of the next ring stage
@@ -495,32 +696,23 @@ __global__ void __launch_bounds__(kOhThreads, 1)
           OH_ACC(2, t0);
         }
         tc_fence_after();
-        if (lane == 0) {
-          const int nk = min(2, p.nkb - 2 * st);
-          for (int kk = 0; kk < nk; ++kk) {
-            const int kb = 2 * st + kk;
-            // descriptor start address advances in 16-byte units: block kb, 32-byte K step j
-            const uint64_t bd = b_desc0 + (uint64_t)((kb * p.NT * kKB) >> 4);
-#pragma unroll
-            for (int j = 0; j < kKB / 32; ++j) {
-              const uint32_t a_tmem = tmem_base + a_col0 + as * kStageCols + kk * 32 + j * 8;
-              if (!(p.debug & 2)) mma_i8_ts(d_tmem, a_tmem, bd + (uint64_t)(j * 2), idesc, (kb | j) != 0);
-            }
-          }
-          tc_commit(&a_empty[as]);
+        if (!(p.debug & 2)) {
+          const uint64_t bd = b_desc0 + (uint64_t)((2 * st * p.NT * kKB) >> 4);
+          const uint32_t a_tmem = tmem_base + a_col0 + as * SC;
+          if constexpr (SP)
+            issue_stage_sp<1>(d_tmem, a_tmem, bd, bstep1, idesc, st != 0, 2 * st + 1 < p.nkb, a_tmem + 32);
+          else
+            issue_stage<1>(d_tmem, a_tmem, bd, bstep1, idesc, st != 0, 2 * st + 1 < p.nkb);
         }
-        __syncwarp();
+        commit_elect(&a_empty[as], false);
         if (++as == nas) {
           as = 0;
           aph ^= 1;
         }
       }
       OH_ACC(3, t_unit);
-      if (lane == 0) {
-        tc_commit(&acc_full[acc]);
-        if (!has_next || nt_next != ntile) tc_commit(b_empty);
-      }
-      __syncwarp();
+      commit_elect(&acc_full[acc], false);
+      if (!has_next || nt_next != ntile) commit_elect(b_empty, false);
       if (++acc == 2) {
         acc = 0;
         accphase ^= 1;
@@ -553,13 +745,17 @@ __global__ void __launch_bounds__(kOhThreads, 1)
       if (p.debug & 8) my_g = unit_end + (my_g & 1);  // MMA-only ablation: generators idle
       StageCodes<K> cur, nxt;
       if (my_g < unit_end) cur.load(row_saddr, sw, (int)(my_g - unit_g));
-      uint32_t w[64];
+      uint32_t w[SP ? 32 : 64];
+      uint32_t we[8];
       for (; my_g < unit_end; my_g += 2) {
         const int st = (int)(my_g - unit_g);
         if (my_g + 2 < unit_end) nxt.load(row_saddr, sw, st + 2);
         {
           OH_T0(t0);
-          build_onehot<K>(cur, w);
+          if constexpr (SP)
+            build_sparse<K>(cur, w, we);
+          else
+            build_onehot<K>(cur, w);
           if (tr) OH_ACC(5, t0);
         }
         {
@@ -570,7 +766,12 @@ __global__ void __launch_bounds__(kOhThreads, 1)
         tc_fence_after();
         if (!(p.debug & 4)) {
           OH_T0(t0);
-          tmem_st64(lane_base + as * kStageCols, w);
+          if constexpr (SP) {
+            tmem_st32(lane_base + as * SC, w);
+            tmem_st8(lane_base + as * SC + 32, we);
+          } else {
+            tmem_st64(lane_base + as * SC, w);
+          }
           tmem_st_wait();
           if (tr) OH_ACC(7, t0);
         }
@@ -792,9 +993,25 @@ __device__ __forceinline__ bool mbar_test_cluster(uint64_t* bar, uint32_t parity
   return ok != 0;
 }
 // latency-critical wait: poll (test_wait) when spin, else sleep in try_wait
+__device__ __forceinline__ bool mbar_try_wait_cluster_nohint(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// spin: 0 = try_wait with a long suspend hint, 1 = test_wait polling,
+// 2 = try_wait with the hardware's default time slice
 __device__ __forceinline__ void mbar_wait_crit(uint64_t* bar, uint32_t parity, int spin) {
-  if (spin) {
+  if (spin == 1) {
     while (!mbar_test_cluster(bar, parity)) {
+    }
+  } else if (spin == 2) {
+    while (!mbar_try_wait_cluster_nohint(bar, parity)) {
     }
   } else {
     mbar_wait_cluster(bar, parity);
@@ -821,65 +1038,14 @@ __device__ __forceinline__ void mma_i8_ts_pair(uint32_t d_tmem, uint32_t a_tmem,
       : "memory");
 }
 
-// One ring stage (up to two 128-byte K blocks = 8 MMAs) issued from a single
-// asm block executed by the whole warp, predicated on elect.sync: operands stay
-// warp-uniform (no per-MMA R2UR/ELECT loop in SASS) and the 8 address offsets
-// are immediates.  acc0 = accumulate flag of the stage's first MMA.
-#define OH_MMA_G(G, AOFF, BOFF, PRED)       \
-  "add.u32 ta, %1, " #AOFF ";\n\t"        \
-  "add.u64 tb, %2, " #BOFF ";\n\t"        \
-  "@e tcgen05.mma.cta_group::" #G ".kind::i8 [%0], [ta], tb, %4, " #PRED ";\n\t"
-#define OH_MMA_H(G, AOFF, BOFF)             \
-  "add.u32 ta, %1, " #AOFF ";\n\t"        \
-  "add.u64 tb, tb2, " #BOFF ";\n\t"       \
-  "@e tcgen05.mma.cta_group::" #G ".kind::i8 [%0], [ta], tb, %4, pt2;\n\t"
-#define OH_STAGE_ASM(G)                                                                      \
-  "{\n\t.reg .pred e, p0, pt2, e2;\n\t.reg .b32 ta;\n\t.reg .b64 tb, tb2;\n\t"            \
-  "elect.sync _|e, 0xffffffff;\n\t"                                                         \
-  "setp.ne.u32 p0, %5, 0;\n\t"                                                              \
-  "setp.eq.u32 pt2, %4, %4;\n\t"                                                            \
-  OH_MMA_G(G, 0, 0, p0) OH_MMA_G(G, 8, 2, pt2) OH_MMA_G(G, 16, 4, pt2) OH_MMA_G(G, 24, 6, pt2) \
-  "setp.ne.u32 e2, %6, 0;\n\t"                                                              \
-  "and.pred e, e, e2;\n\t"                                                                  \
-  "add.u64 tb2, %2, %3;\n\t"                                                                \
-  OH_MMA_H(G, 32, 0) OH_MMA_H(G, 40, 2) OH_MMA_H(G, 48, 4) OH_MMA_H(G, 56, 6) "}"
 
-// One ring stage (up to two 128-byte K blocks = 8 MMAs) issued from a single
-// asm block executed by the whole warp, predicated on elect.sync: operands stay
-// warp-uniform (no per-MMA R2UR/ELECT loop in SASS) and the 8 address offsets
-// are immediates.  acc0 = accumulate flag of the stage's first MMA; two = the
-// stage holds a second K block.
-template <int CG>
-__device__ __forceinline__ void issue_stage(uint32_t d, uint32_t a, uint64_t b, uint64_t bstep, uint32_t idesc,
-                                            uint32_t acc0, uint32_t two) {
-  if constexpr (CG == 2) {
-    asm volatile(OH_STAGE_ASM(2)::"r"(d), "r"(a), "l"(b), "l"(bstep), "r"(idesc), "r"(acc0), "r"(two) : "memory");
-  } else {
-    asm volatile(OH_STAGE_ASM(1)::"r"(d), "r"(a), "l"(b), "l"(bstep), "r"(idesc), "r"(acc0), "r"(two) : "memory");
-  }
-}
 
-// tcgen05.commit from an elected lane (whole warp executes it)
-__device__ __forceinline__ void commit_elect(uint64_t* bar, bool pair) {
-  if (pair)
-    asm volatile(
-        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
-            smem_u32(bar)),
-        "h"((uint16_t)3)
-        : "memory");
-  else
-    asm volatile(
-        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
-        : "memory");
-}
-
-template <int K, int DIGITS>
+template <int K, int DIGITS, int SP, int KB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     onehot_pair_kernel(const __grid_constant__ CUtensorMap codes_map, const __grid_constant__ CUtensorMap out_map,
                        const __grid_constant__ OneHotParams p) {
   static_assert(K >= 4, "K >= 4 on the tensor-core path");
+  constexpr int SC = SP ? (KB * kSparseStageCols) / 2 : kStageCols;  // TMEM columns per A ring stage
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window (LDS, not generic LD)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -907,7 +1073,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   uint64_t* b_ready = bars + 10 + 2 * kMaxAStages;     // leader: peer's B half landed
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(bars + 11 + 2 * kMaxAStages);
   const uint32_t nas = (uint32_t)p.a_stages;
-  const int nst = (p.nkb + 1) >> 1;
+  const int nst = (p.nkb + KB - 1) / KB;  // ring stages per unit
 
   if (threadIdx.x == 0) {
     mbar_init(b_full, 1);
@@ -922,7 +1088,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     for (int i = 0; i < p.a_stages; ++i) {
       // leader: its 4 generator warps + 1 forward from the peer's signaler;
       // peer: its 4 generator warps (collected locally, then forwarded)
-      mbar_init(&a_full[i], leader ? 5 : 4);
+      mbar_init(&a_full[i], (leader && !(p.debug & 16)) ? 5 : 4);  // debug 16: leader ignores the peer
       mbar_init(&a_empty[i], 1);
     }
     fence_mbar_init();
@@ -999,10 +1165,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     int64_t rt;
     while (walk.next(ntile, rt)) {
       for (int st = 0; st < nst; ++st) {
-        mbar_wait_crit(&a_full[as], aph, p.spin);
+        mbar_wait_crit(&a_full[as], aph, p.spin == 3 ? 1 : p.spin);
         tc_fence_after();
         tc_fence_before();
-        if (lane == 0) mbar_arrive_cluster(a_full_l + as * 8);
+        if (lane == 0 && !(p.debug & 16)) mbar_arrive_cluster(a_full_l + as * 8);
         __syncwarp();
         if (++as == nas) {
           as = 0;
@@ -1013,7 +1179,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (leader only)
     if (leader) {
-      const uint32_t idesc = idesc_i8(256, NN);
+      const uint32_t idesc = idesc_i8(256, NN) | (SP ? 4u : 0u);  // bit 2: sparse A
       int cur_ntile = -1;
       uint32_t b_phase = 0;
       uint32_t as = 0, aph = 0;
@@ -1050,13 +1216,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int st = 0; st < nst; ++st) {
           {
             OH_T0(t0);
-            mbar_wait_crit(&a_full[as], aph, p.spin);
+            mbar_wait_crit(&a_full[as], aph, p.spin == 3 ? 1 : p.spin);
             OH_ACC(2, t0);
           }
           tc_fence_after();
-          if (!(p.debug & 2))
-            issue_stage<2>(d_tmem, a_col0 + as * kStageCols, b_desc0 + (uint64_t)((2 * st * NH * kKB) >> 4),
-                           bstep, idesc, st != 0, 2 * st + 1 < p.nkb);
+          if (!(p.debug & 2)) {
+            if constexpr (SP && KB == 1)
+              issue_stage_sp1<2>(d_tmem, a_col0 + as * SC, b_desc0 + (uint64_t)((st * NH * kKB) >> 4), idesc, st != 0,
+                                 a_col0 + as * SC + 16);
+            else if constexpr (SP)
+              issue_stage_sp<2>(d_tmem, a_col0 + as * SC, b_desc0 + (uint64_t)((2 * st * NH * kKB) >> 4), bstep,
+                                idesc, st != 0, 2 * st + 1 < p.nkb, a_col0 + as * SC + 32);
+            else
+              issue_stage<2>(d_tmem, a_col0 + as * SC, b_desc0 + (uint64_t)((2 * st * NH * kKB) >> 4), bstep,
+                             idesc, st != 0, 2 * st + 1 < p.nkb);
+          }
           commit_elect(&a_empty[as], true);
           if (++as == nas) {
             as = 0;
@@ -1095,20 +1269,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       }
       const uint32_t row_saddr = smem_u32(code_smem + cs * code_tile_bytes) + row_in_tile * 128;
       const uint32_t unit_end = unit_g + nst;
-      StageCodes<K> cur, nxt;
+      StageCodes<K, KB> cur, nxt;
       if (my_g < unit_end) cur.load(row_saddr, sw, (int)(my_g - unit_g));
-      uint32_t w[64];
+      uint32_t w[SP ? 16 * KB : 64];
+      uint32_t we[4 * KB];
       for (; my_g < unit_end; my_g += 2) {
         const int st = (int)(my_g - unit_g);
         if (my_g + 2 < unit_end) nxt.load(row_saddr, sw, st + 2);
         long long t0 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
-        build_onehot<K>(cur, w);
+        if constexpr (SP)
+          build_sparse<K, KB>(cur, w, we);
+        else
+          build_onehot<K>(cur, w);
         long long t1 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
-        mbar_wait(&a_empty[as], aph ^ 1);
+        mbar_wait_crit(&a_empty[as], aph ^ 1, p.spin == 3 ? 0 : p.spin);  // spin 3: only MMA/signaler poll
         long long t2 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
         tc_fence_after();
         if (!(p.debug & 4)) {
-          tmem_st64(lane_base + as * kStageCols, w);
+          if constexpr (SP && KB == 1) {
+            tmem_st16(lane_base + as * SC, w);
+            tmem_st4(lane_base + as * SC + 16, we);
+          } else if constexpr (SP) {
+            tmem_st32(lane_base + as * SC, w);
+            tmem_st8(lane_base + as * SC + 32, we);
+          } else {
+            tmem_st64(lane_base + as * SC, w);
+          }
           tmem_st_wait();
         }
         long long t3 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
@@ -1456,7 +1642,7 @@ const double* onehot_col_scale(const void* image, int C, int K, int M, int digit
 template <int K, int DIGITS>
 static int launch_onehot_k(const CUtensorMap& map, const CUtensorMap& omap, OneHotParams& p, size_t smem, int grid,
                            cudaStream_t stream) {
-  auto kern = onehot_gemm_kernel<K, DIGITS>;
+  auto kern = p.sparse ? onehot_gemm_kernel<K, DIGITS, 1> : onehot_gemm_kernel<K, DIGITS, 0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(onehot)");
   kern<<<grid, kOhThreads, smem, stream>>>(map, omap, p);
@@ -1467,7 +1653,8 @@ static int launch_onehot_k(const CUtensorMap& map, const CUtensorMap& omap, OneH
 template <int K, int DIGITS>
 static int launch_pair_k(const CUtensorMap& map, const CUtensorMap& omap, OneHotParams& p, size_t smem, int grid,
                          cudaStream_t stream) {
-  auto kern = onehot_pair_kernel<K, DIGITS>;
+  auto kern = !p.sparse ? onehot_pair_kernel<K, DIGITS, 0, 2>
+               : p.stage_kb == 1 ? onehot_pair_kernel<K, DIGITS, 1, 1> : onehot_pair_kernel<K, DIGITS, 1, 2>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(onehot_pair)");
   kern<<<grid, kPairThreads, smem, stream>>>(map, omap, p);
@@ -1541,25 +1728,36 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
     const char* dbg = getenv("LUTGPU_OH_DEBUG");
     p.debug = dbg ? atoi(dbg) : 0;
   }
-  if (g.pair) {
+  const char* pair_env = getenv("LUTGPU_OH_PAIR");
+  if (g.pair && !(pair_env && pair_env[0] == '0')) {
     // ---------------- CTA-pair kernel: MMA N = 2*NT, 256-row pair tiles
     const int NN = 2 * g.NT;
     p.ntiles = g.ntiles / 2;
     p.MT = NN / digits;
     p.nrt = (n + 2 * kRowsPerTile - 1) / (2 * kRowsPerTile);
     p.n_acc = 2;
-    p.spin = 0;
+    p.spin = 3;  // MMA issuer and peer signaler poll their critical barriers; generators sleep
     {
       const char* e1 = getenv("LUTGPU_OH_ACC1");
       if (e1 && e1[0] == '1') p.n_acc = 1;
       const char* e2 = getenv("LUTGPU_OH_SPIN");
-      if (e2 && e2[0] == '1') p.spin = 1;
+      if (e2) p.spin = atoi(e2);
     }
-    p.a_stages = (512 - p.n_acc * NN) / 64;
+    {
+      const char* e3 = getenv("LUTGPU_OH_DENSE");
+      p.sparse = (e3 && e3[0] == '1') ? 0 : 1;
+    }
+    p.stage_kb = 2;
+    {
+      const char* e4 = getenv("LUTGPU_OH_KB");
+      if (e4 && e4[0] == '1') p.stage_kb = 1;
+    }
+    const int sc = p.sparse ? (p.stage_kb * kSparseStageCols) / 2 : kStageCols;
+    p.a_stages = ((512 - p.n_acc * NN) / sc) & ~1;  // even: the two generator groups own alternate stages
     if (p.a_stages > kMaxAStages) p.a_stages = kMaxAStages;
     if (p.a_stages < 2) return fail(LUT_ERR_CONFIG, "one-hot gather: TMEM budget exceeded");
     uint32_t alloc = 32;
-    while (alloc < (uint32_t)(p.n_acc * NN + p.a_stages * 64)) alloc <<= 1;
+    while (alloc < (uint32_t)(p.n_acc * NN + p.a_stages * sc)) alloc <<= 1;
     p.tmem_cols = alloc;
     const int nsm = num_sms();
     const int64_t units = (int64_t)p.ntiles * p.nrt;
@@ -1575,7 +1773,7 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
     if (p.band_rt > p.nrt) p.band_rt = p.nrt;
     const size_t b_bytes = (size_t)g.NT * g.nkb * kKB;
     const size_t base_smem =
-        ((b_bytes + 1023) & ~size_t(1023)) + 2 * (size_t)code_boxes * kRowsPerTile * 128 + 256 + 1024;
+        ((b_bytes + 1023) & ~size_t(1023)) + 2 * (size_t)code_boxes * kRowsPerTile * 128 + 512 + 1024;
     if (base_smem > max_smem_optin()) return fail(LUT_ERR_CONFIG, "one-hot gather: shared memory budget exceeded");
     const int half_cols = p.MT / 2;
     const int ib = half_cols < 32 ? half_cols : 32;
@@ -1619,15 +1817,21 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
       default: return fail(LUT_ERR_CONFIG, "digits must be 1, 2 or 4");
     }
   }
-  // TMEM: 2 accumulators (2*NT columns) + the A ring (64 columns per stage)
-  p.a_stages = (512 - 2 * g.NT) / 64;
+  // TMEM: 2 accumulators (2*NT columns) + the A ring (64 dense / 40 sparse columns per stage);
+  // an even ring depth (the two generator warp groups own alternate stages)
+  {
+    const char* e3 = getenv("LUTGPU_OH_DENSE");
+    p.sparse = (e3 && e3[0] == '1') ? 0 : 1;
+  }
+  const int sc1 = p.sparse ? kSparseStageCols : kStageCols;
+  p.a_stages = ((512 - 2 * g.NT) / sc1) & ~1;
   if (p.a_stages > kMaxAStages) p.a_stages = kMaxAStages;
   if (p.a_stages < 2) return fail(LUT_ERR_CONFIG, "one-hot gather: TMEM budget exceeded");
   {
     const char* st = getenv("LUTGPU_OH_ASTAGES");
     if (st && atoi(st) >= 2 && atoi(st) <= p.a_stages) p.a_stages = atoi(st);
   }
-  uint32_t cols = 2 * g.NT + p.a_stages * 64;
+  uint32_t cols = 2 * g.NT + p.a_stages * sc1;
   uint32_t alloc = 32;
   while (alloc < cols) alloc <<= 1;
   p.tmem_cols = alloc;
@@ -1650,7 +1854,7 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
   if (p.band_rt > p.nrt) p.band_rt = p.nrt;
   const size_t b_bytes = (size_t)g.NT * g.nkb * kKB;
   const size_t base_smem =
-      ((b_bytes + 1023) & ~size_t(1023)) + 2 * (size_t)code_boxes * kRowsPerTile * 128 + 256 + 1024;
+      ((b_bytes + 1023) & ~size_t(1023)) + 2 * (size_t)code_boxes * kRowsPerTile * 128 + 512 + 1024;
   if (base_smem > max_smem_optin()) return fail(LUT_ERR_CONFIG, "one-hot gather: shared memory budget exceeded");
   // TMA-store epilogue: row-major f32 out, 16-byte row pitch, staging fits
   const size_t stage_bytes = 2 * (size_t)kRowsPerTile * g.MT * 4;

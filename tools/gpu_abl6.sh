@@ -1,0 +1,6 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+for cfg in "LUTGPU_OH_DEBUG=7" "LUTGPU_OH_DEBUG=71" "LUTGPU_OH_DEBUG=135" "LUTGPU_OH_DEBUG=199" "LUTGPU_OH_DEBUG=15" "LUTGPU_OH_DEBUG=79"; do
+  env $cfg timeout 120 python bench.py --no-cpu --no-e2e --steps 5 > gpurun_out/abl6.json 2>/dev/null
+  python -c "import json;d=json.load(open('gpurun_out/abl6.json'));print('$cfg', 'gather_ms', round(d['roofline']['kernel_ms']['gather'],3))" 2>/dev/null || echo "$cfg failed"
+done
