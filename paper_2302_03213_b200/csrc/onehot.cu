@@ -14,19 +14,20 @@
 // far inside the fp32 contract (rtol/atol 1e-5, BASELINE north star); the
 // bitwise ascending-c fp32 path remains in gather.cu.
 //
-// Kernel anatomy (one persistent CTA per SM, 12 warps):
+// Kernel anatomy (single-CTA variant: one persistent CTA per SM, 14 warps):
 //   warp 0      producer: bulk-copies the prepared B image of the current
 //               n-tile (resident in SMEM, reloaded only when the n-tile
 //               changes) and TMA-loads 128-row code tiles (128B swizzle).
 //   warp 1      TMEM allocator + MMA issuer (one elected lane):
-//               tcgen05.mma.cta_group::1.kind::i8, A from TMEM, B from SMEM.
-//   warps 4-7   one-hot generators: thread = row = TMEM lane; builds the
-//               row's one-hot bytes for a 128-byte K block in registers and
-//               tcgen05.st's them into a 4-stage A ring in TMEM (the A
-//               operand never touches shared memory).
-//   warps 8-11  epilogue: tcgen05.ld the int32 accumulator (double
+//               tcgen05.mma.cta_group::1.kind::i8 (or .sp), A from TMEM, B from SMEM.
+//   warps 2-9   one-hot generators: thread = row = TMEM lane (quarter warp%4);
+//               builds the row's (2:4-compressed) one-hot bytes in registers
+//               and tcgen05.st's them into the A ring in TMEM (the A operand
+//               never touches shared memory).
+//   warps 10-13 epilogue: tcgen05.ld the int32 accumulator (double
 //               buffered in TMEM), scale (+digit recombination), bias, act,
-//               128-bit stores.
+//               swizzled SMEM staging + TMA store.
+// The CTA-pair kernel (below) is the configs[4] fast path.
 // Work = (n-tile, 128-row tile) units, walked in row bands so every CTA works
 // near the same rows (codes stay in L2) while each CTA keeps one n-tile's B
 // image for many consecutive row tiles.
@@ -35,7 +36,7 @@
 
 namespace lutgpu {
 
-constexpr int kOhThreads = 16 * 32;
+constexpr int kOhThreads = 14 * 32;  // producer, MMA, 8 generators, 4 epilogue
 constexpr int kRowsPerTile = 128;
 constexpr int kKB = 128;       // K bytes per A stage / B block
 constexpr int kMaxAStages = 24;  // A ring depth bound (barrier arrays)
@@ -138,6 +139,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       "%15}, [%16];"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16_lo(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr)
       : "memory");
 }
@@ -261,6 +272,7 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // Code bytes of one ring stage (two 128-byte K blocks) for this row, read
@@ -551,9 +563,11 @@ __device__ __forceinline__ void commit_elect(uint64_t* bar, bool pair) {
     if (p.trace && blockIdx.x == 0 && lane == 0) atomicAdd(p.trace + (slot), (unsigned long long)(clock64() - var)); \
   } while (0)
 
-constexpr int kGenWarp0 = 4;   // warps 4..11: generators (parity = (warp-4)>>2)
-constexpr int kEpiWarp0 = 12;  // warps 12..15: epilogue (pair kernel: 12..19, one accumulator half each)
-constexpr int kPairThreads = 20 * 32;
+// Role warps.  A warp may only touch the TMEM lane quarter warp % 4, so each
+// group of 4 consecutive warps covers all 128 rows whatever its first index.
+constexpr int kGenWarp0 = 2;   // warps 2..9: generators (parity = (warp-2)>>2)
+constexpr int kEpiWarp0 = 10;  // warps 10..13: epilogue (pair kernel: 10..17, one accumulator half each)
+constexpr int kPairThreads = 18 * 32;
 constexpr int kGenWarps = 8;
 constexpr int kStageCols = 64;  // TMEM columns per A stage (2 K blocks x 128 B / 4 B)
 constexpr int kSparseStageCols = 40;  // 2:4 sparse stage: 32 compressed A + 8 metadata columns
@@ -1221,7 +1235,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           }
           tc_fence_after();
           if (!(p.debug & 2)) {
-            if constexpr (SP && KB == 1)
+            if constexpr (SP && KB == 4) {
+              const uint64_t bst = b_desc0 + (uint64_t)((4 * st * NH * kKB) >> 4);
+              const uint32_t abase = a_col0 + as * SC;
+              issue_stage_sp<2>(d_tmem, abase, bst, bstep, idesc, st != 0, 4 * st + 1 < p.nkb, abase + 64);
+              if (4 * st + 2 < p.nkb)
+                issue_stage_sp<2>(d_tmem, abase + 32, bst + 2 * bstep, bstep, idesc, 1, 4 * st + 3 < p.nkb,
+                                  abase + 72);
+            } else if constexpr (SP && KB == 1)
               issue_stage_sp1<2>(d_tmem, a_col0 + as * SC, b_desc0 + (uint64_t)((st * NH * kKB) >> 4), idesc, st != 0,
                                  a_col0 + as * SC + 16);
             else if constexpr (SP)
@@ -1269,16 +1290,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       }
       const uint32_t row_saddr = smem_u32(code_smem + cs * code_tile_bytes) + row_in_tile * 128;
       const uint32_t unit_end = unit_g + nst;
-      StageCodes<K, KB> cur, nxt;
+      if constexpr (SP && KB == 4) {
+        // 4 K blocks per stage, built and stored as two halves (register budget)
+        const int nsub = (p.nkb + 1) >> 1;
+        for (; my_g < unit_end; my_g += 2) {
+          const int st = (int)(my_g - unit_g);
+          StageCodes<K, 2> c0, c1;
+          const bool has1 = 2 * st + 1 < nsub;
+          c0.load(row_saddr, sw, 2 * st);
+          if (has1) c1.load(row_saddr, sw, 2 * st + 1);
+          uint32_t w[32], we[8];
+          build_sparse<K, 2>(c0, w, we);
+          mbar_wait_crit(&a_empty[as], aph ^ 1, p.spin == 3 ? 0 : p.spin);
+          tc_fence_after();
+          if (!(p.debug & 4)) {
+            tmem_st32(lane_base + as * SC, w);
+            tmem_st8(lane_base + as * SC + 64, we);
+          }
+          if (has1) {
+            build_sparse<K, 2>(c1, w, we);
+            if (!(p.debug & 4)) {
+              tmem_st32(lane_base + as * SC + 32, w);
+              tmem_st8(lane_base + as * SC + 72, we);
+            }
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&a_full[as]);
+          as += 2;
+          if (as >= nas) {
+            as -= nas;
+            aph ^= 1;
+          }
+        }
+      } else {
+      StageCodes<K, KB == 4 ? 2 : KB> cur, nxt;
       if (my_g < unit_end) cur.load(row_saddr, sw, (int)(my_g - unit_g));
-      uint32_t w[SP ? 16 * KB : 64];
-      uint32_t we[4 * KB];
+      uint32_t w[SP ? 16 * (KB == 4 ? 2 : KB) : 64];
+      uint32_t we[4 * (KB == 4 ? 2 : KB)];
       for (; my_g < unit_end; my_g += 2) {
         const int st = (int)(my_g - unit_g);
         if (my_g + 2 < unit_end) nxt.load(row_saddr, sw, st + 2);
         long long t0 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
         if constexpr (SP)
-          build_sparse<K, KB>(cur, w, we);
+          build_sparse<K, KB == 4 ? 2 : KB>(cur, w, we);
         else
           build_onehot<K>(cur, w);
         long long t1 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
@@ -1313,6 +1369,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           aph ^= 1;
         }
       }
+      }
       unit_g = unit_end;
       __syncwarp();
       if (lane == 0) mbar_arrive(&code_empty[cs]);
@@ -1334,8 +1391,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const int ib_log2 = 31 - __clz(ib);
     const int swz = ib == 32 ? (row_in_tile & 7) : ib == 16 ? ((row_in_tile >> 1) & 3) : ib == 8 ? ((row_in_tile >> 2) & 1) : 0;
     const float scale0 = (DIGITS == 1 && p.scales) ? __ldg(p.scales) : 1.0f;
+    const bool etr = p.trace && blockIdx.x == 0 && warp == kEpiWarp0 && lane == 0;
     while (walk.next(ntile, rt)) {
+      long long e0 = etr ? clock64() : 0;
       mbar_wait(&acc_full[acc], accphase);
+      long long e1 = etr ? clock64() : 0;
       tc_fence_after();
       const int64_t row0 = rt * 2 * kRowsPerTile + rank * kRowsPerTile;
       const int64_t row = row0 + row_in_tile;
@@ -1344,18 +1404,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       {
         const int hf = (warp - kEpiWarp0) >> 2;  // this warp's accumulator half
         const int HC = NN / 2;  // accumulator columns of this half (16, 32 or 64)
-        uint32_t v[64];
+        // two passes of 32 accumulator columns (registers: v[32], not v[64]);
+        // the accumulator half is released after its last load
+        uint32_t v[32];
+        const int pc = HC >= 32 ? 32 : 16;  // columns per pass
+        const int npass = HC / pc;
+        long long e2 = etr ? clock64() : 0;
+        long long e3 = e2;
+        if (!(p.debug & 1) && p.tma_out) {
+          if (lane == 0) bulk_wait_read0();  // this warp's single staging slab: previous store fully read
+          __syncwarp();
+        }
+        const uint32_t out_saddr = smem_u32(stage_out + hf * half_bytes) + row_in_tile * (ib * 4);
+        for (int h2 = 0; h2 < npass; ++h2) {
         {
-          const uint32_t tb = tmem_base + ((uint32_t)(sub * 32) << 16) + acc * NN + hf * HC;
-          if (HC >= 32) {
-            tmem_ld32_at<0>(tb, v);
-            if (HC == 64) tmem_ld32_at<32>(tb + 32, v);
-          } else {
-            tmem_ld16_at<0>(tb, v);
-          }
+          const uint32_t tb = tmem_base + ((uint32_t)(sub * 32) << 16) + acc * NN + hf * HC + h2 * 32;
+          if (pc == 32)
+            tmem_ld32(tb, v);
+          else
+            tmem_ld16_lo(tb, v);
           tmem_ld_wait();
         }
-        {
+        if (h2 == npass - 1) {
           // this warp's half of the accumulator is in registers: release it
           tc_fence_before();
           if (leader) {
@@ -1366,17 +1436,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             if (elected) mbar_arrive_cluster(acc_empty_l + acc * 8);
           }
         }
-        if (!(p.debug & 1)) {
-        // each warp stages and TMA-stores its own 32-row slab (box {ib, 32})
-        if (p.tma_out) {
-          if (lane == 0) bulk_wait_read1();  // this warp's slab of half hf (one unit ago) is free
-          __syncwarp();
-        }
-        const uint32_t out_saddr = smem_u32(stage_out + hf * half_bytes) + row_in_tile * (ib * 4);
+        if (p.debug & 1) continue;
 #pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) {
-          const int ch = c4 * 16;
-          if (ch >= HC) break;
+        for (int c4 = 0; c4 < 2; ++c4) {
+          const int cl = c4 * 16;   // column inside this pass (v index)
+          if (cl >= pc) break;
+          const int ch = h2 * 32 + cl;  // column inside this half
           constexpr int RC = 16 / DIGITS;
           const int mc = m_base + (hf * HC + ch) / DIGITS;
           const bool full_chunk = mc + RC <= p.M;
@@ -1388,25 +1453,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 const int m = mc + j;
                 if (m < p.M)
                   p.out_i32[p.out_hw > 0 ? ((row / p.out_hw) * p.M + m) * p.out_hw + row % p.out_hw : row * p.M + m] =
-                      (int)v[ch + j];
+                      (int)v[cl + j];
               }
             }
             if (p.scale_mtile > 0) {
 #pragma unroll
               for (int j = 0; j < RC; ++j) {
                 const int m = mc + j;
-                f[j] = __fmul_rn(__int2float_rn((int)v[ch + j]), m < p.M ? __ldg(p.scales + m / p.scale_mtile) : 1.0f);
+                f[j] = __fmul_rn(__int2float_rn((int)v[cl + j]), m < p.M ? __ldg(p.scales + m / p.scale_mtile) : 1.0f);
               }
             } else {
 #pragma unroll
-              for (int j = 0; j < RC; ++j) f[j] = __fmul_rn(i2f_exact(v[ch + j]), scale0);
+              for (int j = 0; j < RC; ++j) f[j] = __fmul_rn(i2f_exact(v[cl + j]), scale0);
             }
           } else {
 #pragma unroll
             for (int j = 0; j < RC; ++j) {
               long long t = 0;
 #pragma unroll
-              for (int dg = DIGITS - 1; dg >= 0; --dg) t = t * 256 + (long long)(int)v[ch + j * DIGITS + dg];
+              for (int dg = DIGITS - 1; dg >= 0; --dg) t = t * 256 + (long long)(int)v[cl + j * DIGITS + dg];
               const int m = mc + j;
               const double sc = m < p.M ? __ldg(p.col_scale + m) : 0.0;
               f[j] = (float)((double)t * sc);
@@ -1460,7 +1525,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             }
           }
         }
-        if (p.tma_out && p.out && !(p.debug & 48)) {
+        }  // passes
+        e3 = etr ? clock64() : 0;
+        if (p.tma_out && p.out && !(p.debug & 49)) {
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -1470,7 +1537,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             bulk_commit();
           }
         }
-        }  // !(debug & 1)
+        // end of epilogue body
+
+        if (etr) {
+          const long long e4 = clock64();
+          atomicAdd(p.trace + 8, (unsigned long long)(e1 - e0));
+          atomicAdd(p.trace + 9, (unsigned long long)(e2 - e1));
+          atomicAdd(p.trace + 10, (unsigned long long)(e3 - e2));
+          atomicAdd(p.trace + 11, (unsigned long long)(e4 - e3));
+        }
       }
       if (++acc == p.n_acc) {
         acc = 0;
@@ -1653,8 +1728,10 @@ static int launch_onehot_k(const CUtensorMap& map, const CUtensorMap& omap, OneH
 template <int K, int DIGITS>
 static int launch_pair_k(const CUtensorMap& map, const CUtensorMap& omap, OneHotParams& p, size_t smem, int grid,
                          cudaStream_t stream) {
-  auto kern = !p.sparse ? onehot_pair_kernel<K, DIGITS, 0, 2>
-               : p.stage_kb == 1 ? onehot_pair_kernel<K, DIGITS, 1, 1> : onehot_pair_kernel<K, DIGITS, 1, 2>;
+  auto kern = !p.sparse            ? onehot_pair_kernel<K, DIGITS, 0, 2>
+              : p.stage_kb == 1 ? onehot_pair_kernel<K, DIGITS, 1, 1>
+              : p.stage_kb == 4 ? onehot_pair_kernel<K, DIGITS, 1, 4>
+                                : onehot_pair_kernel<K, DIGITS, 1, 2>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(onehot_pair)");
   kern<<<grid, kPairThreads, smem, stream>>>(map, omap, p);
@@ -1747,13 +1824,13 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
       const char* e3 = getenv("LUTGPU_OH_DENSE");
       p.sparse = (e3 && e3[0] == '1') ? 0 : 1;
     }
-    p.stage_kb = 2;
+    p.stage_kb = 4;  // 4 K blocks (8 sparse MMAs) per ring handshake
     {
       const char* e4 = getenv("LUTGPU_OH_KB");
-      if (e4 && e4[0] == '1') p.stage_kb = 1;
+      if (e4 && (e4[0] == '1' || e4[0] == '2' || e4[0] == '4')) p.stage_kb = e4[0] - '0';
     }
     const int sc = p.sparse ? (p.stage_kb * kSparseStageCols) / 2 : kStageCols;
-    p.a_stages = ((512 - p.n_acc * NN) / sc) & ~1;  // even: the two generator groups own alternate stages
+    p.a_stages = (512 - p.n_acc * NN) / sc;  // generator groups take alternate global stages (any depth >= 2)
     if (p.a_stages > kMaxAStages) p.a_stages = kMaxAStages;
     if (p.a_stages < 2) return fail(LUT_ERR_CONFIG, "one-hot gather: TMEM budget exceeded");
     uint32_t alloc = 32;
@@ -1802,7 +1879,7 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
         cudaMemcpy(h, t, sizeof(h), cudaMemcpyDeviceToHost);
         const char* names[16] = {"L.mma.wait_b", "L.mma.wait_acc_empty", "L.mma.wait_a_full", "L.mma.unit",
                                  "L.gen.wait_code", "L.gen.build", "L.gen.wait_a_empty", "L.gen.st",
-                                 "-", "-", "-", "-", "P.gen.wait_code", "P.gen.build", "P.gen.wait_a_empty", "P.gen.st"};
+                                 "L.epi.wait_acc", "L.epi.ld", "L.epi.math", "L.epi.store", "P.gen.wait_code", "P.gen.build", "P.gen.wait_a_empty", "P.gen.st"};
         fprintf(stderr, "[pair trace, %d units]", units);
         for (int i = 0; i < 16; ++i)
           if (names[i][0] != '-') fprintf(stderr, " %s=%.0f", names[i], (double)h[i] / units);
