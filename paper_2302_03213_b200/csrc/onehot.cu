@@ -186,6 +186,26 @@ __device__ __forceinline__ float i2f_exact(uint32_t x) {
   return __fsub_rn(__int_as_float(0x4B400000 + (int)x), 12582912.0f);
 }
 
+__device__ __forceinline__ uint64_t pk_f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void up_f2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t add_f2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t mul_f2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+constexpr uint64_t kNegMagic2 = 0xCB400000CB400000ull;  // {-12582912.0f, -12582912.0f}
+
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // SMEM matrix descriptor: K-major, 128B swizzle, 8-row atoms 1024 B apart.
@@ -1391,6 +1411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const int ib_log2 = 31 - __clz(ib);
     const int swz = ib == 32 ? (row_in_tile & 7) : ib == 16 ? ((row_in_tile >> 1) & 3) : ib == 8 ? ((row_in_tile >> 2) & 1) : 0;
     const float scale0 = (DIGITS == 1 && p.scales) ? __ldg(p.scales) : 1.0f;
+    const uint64_t scale2 = pk_f2(scale0, scale0);
     const bool etr = p.trace && blockIdx.x == 0 && warp == kEpiWarp0 && lane == 0;
     while (walk.next(ntile, rt)) {
       long long e0 = etr ? clock64() : 0;
@@ -1464,7 +1485,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
               }
             } else {
 #pragma unroll
-              for (int j = 0; j < RC; ++j) f[j] = __fmul_rn(i2f_exact(v[cl + j]), scale0);
+              for (int j = 0; j < RC; j += 2) {  // packed FADD2/FMUL2: same two IEEE ops per value
+                const uint64_t big = pk_f2(__int_as_float(0x4B400000 + (int)v[cl + j]),
+                                           __int_as_float(0x4B400000 + (int)v[cl + j + 1]));
+                const uint64_t r = mul_f2(add_f2(big, kNegMagic2), scale2);
+                up_f2(r, f[j], f[j + 1]);
+              }
             }
           } else {
 #pragma unroll
@@ -1517,11 +1543,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                      f[4 * j + 3]);
             }
           } else if (live) {
+            if (p.out_hw == 0 && (RC % 4) == 0 && (p.M & 3) == 0 && full_chunk) {
+              // direct 128-bit stores: this row's RC contiguous outputs
+              float4* dst = reinterpret_cast<float4*>(p.out + row * p.M + mc);
 #pragma unroll
-            for (int j = 0; j < RC; ++j) {
-              const int m = mc + j;
-              if (m < p.M)
-                p.out[p.out_hw > 0 ? ((row / p.out_hw) * p.M + m) * p.out_hw + row % p.out_hw : row * p.M + m] = f[j];
+              for (int j = 0; j < RC / 4; ++j) dst[j] = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < RC; ++j) {
+                const int m = mc + j;
+                if (m < p.M)
+                  p.out[p.out_hw > 0 ? ((row / p.out_hw) * p.M + m) * p.out_hw + row % p.out_hw : row * p.M + m] = f[j];
+              }
             }
           }
         }
@@ -1858,8 +1891,9 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
     CUtensorMap omap;
     memset(&omap, 0, sizeof(omap));
     p.tma_out = 0;
-    if (out && out_hw == 0 && (M % 4) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && ib >= 4 &&
-        half_cols % ib == 0 && base_smem + stage_bytes <= max_smem_optin()) {
+    const char* e5 = getenv("LUTGPU_OH_TMAOUT");
+    if (!(e5 && e5[0] == '0') && out && out_hw == 0 && (M % 4) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+        ib >= 4 && half_cols % ib == 0 && base_smem + stage_bytes <= max_smem_optin()) {
       if (make_tmap_2d_f32_box(&omap, out, (uint64_t)M, (uint64_t)n, (uint32_t)ib, 32)) p.tma_out = 1;
     }
     const size_t smem = base_smem + (p.tma_out ? stage_bytes : 0);
