@@ -43,17 +43,29 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = True) -> str:
+    """Compile stale objects (in parallel; an object is stale when its source,
+    a shared header or the ABI header is newer) and relink the library."""
     if not force and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    objs = []
+    shared = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "lutgpu.h")]
+    objs, procs = [], []
     for src in SOURCES:
         obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
+        objs.append(obj)
+        deps = [os.path.join(CSRC, src)] + shared
+        if not force and os.path.exists(obj) and all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in deps):
+            continue
         cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
-        objs.append(obj)
+        procs.append((obj, subprocess.Popen(cmd)))
+    failed = [obj for obj, pr in procs if pr.wait() != 0]
+    if failed:
+        for obj in failed:
+            if os.path.exists(obj):
+                os.remove(obj)
+        raise subprocess.CalledProcessError(1, f"nvcc ({', '.join(os.path.basename(o) for o in failed)})")
     # export only the extern "C" symbols (visibility=hidden + explicit list via version script)
     vscript = os.path.join(LIBDIR, "exports.map")
     with open(vscript, "w") as f:
@@ -63,8 +75,6 @@ def build(force: bool = False, verbose: bool = True) -> str:
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    for o in objs:
-        os.remove(o)
     return LIB
 
 

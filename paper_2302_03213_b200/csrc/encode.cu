@@ -107,13 +107,12 @@ __device__ __noinline__ int exact_argmin(GetA get_a, const float* __restrict__ c
 
 // --------------------------------------------------------------- TMA path
 
-constexpr int kEncWarps = 8;                  // consumer warps; a broadcast LDS.128 of a centroid costs
-                                              // 4 SMEM wavefronts, so each feeds kRPL rows
-constexpr int kEncThreads = (kEncWarps + 1) * 32;
+// Consumer geometry: W consumer warps x RPL rows per lane = one 512-row tile.
+// A broadcast LDS.128 of a centroid costs 4 SMEM wavefronts whatever the
+// address pattern, so the centroid traffic per (row, k) is 1/RPL of a
+// wavefront per lane: RPL = 4 (4 warps) halves it against RPL = 2 (8 warps).
 constexpr int kBoxRows = 256;                 // TMA box rows
-constexpr int kRPL = 2;                       // rows per lane
-constexpr int kRowsPerPass = kEncWarps * 32;  // rows covered by one pass of all consumer lanes
-constexpr int kTileRows = kRowsPerPass * kRPL;  // 512
+constexpr int kTileRows = 512;
 constexpr int kTileBoxes = kTileRows / kBoxRows;  // A boxes per stage
 constexpr int kBoxBytes = kBoxRows * 128;     // 32 KB (32 f32 columns)
 
@@ -152,9 +151,11 @@ __device__ __forceinline__ void store_code_group(uint8_t* dst, uint32_t w0, uint
   for (int i = 0; i < nbytes; ++i) dst[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
 }
 
-template <int V>
-__global__ void __launch_bounds__(kEncThreads, 1)
+template <int V, int kEncWarps, int kRPL>
+__global__ void __launch_bounds__((kEncWarps + 1) * 32, 1)
     encode_tma_kernel(const __grid_constant__ CUtensorMap tmap, const EncTmaParams p) {
+  constexpr int kRowsPerPass = kEncWarps * 32;  // rows covered by one pass of all consumer lanes
+  static_assert(kRowsPerPass * kRPL == kTileRows, "tile geometry");
   constexpr int NB = 32 / V;   // codebooks per 32-column box
   constexpr int NJ = V / 4;    // 16-byte chunks per sub-vector
   extern __shared__ uint8_t smem_raw[];
@@ -797,10 +798,14 @@ static int launch_tma(const float* a, int64_t n, int d, const float* prep, int C
   const int64_t nunits = p.ntiles * p.ngroups;
   const int grid = (int)(nunits < nsm ? nunits : nsm);
   const size_t smem = (size_t)stages * stage_bytes + 2 * stages * sizeof(uint64_t) + 1024;
-  auto kern = encode_tma_kernel<V>;
+  // rows per lane (LUTGPU_ENC_RPL = 2 or 4; default 4)
+  int rpl = 4;
+  if (const char* r = getenv("LUTGPU_ENC_RPL")) rpl = atoi(r) == 2 ? 2 : 4;
+  auto kern = rpl == 2 ? encode_tma_kernel<V, 8, 2> : encode_tma_kernel<V, 4, 4>;
+  const int threads = rpl == 2 ? 9 * 32 : 5 * 32;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(encode_tma)");
-  kern<<<grid, kEncThreads, smem, stream>>>(tmap, p);
+  kern<<<grid, threads, smem, stream>>>(tmap, p);
   LUT_CHECK_LAUNCH("encode_tma_kernel");
   *used = true;
   return LUT_OK;

@@ -65,7 +65,9 @@ struct OneHotParams {
   int n_acc;                // TMEM accumulator buffers (pair kernel: 1 or 2)
   int spin;                 // 1: latency-critical waits poll instead of sleeping
   int tma_out;              // 1: epilogue stages the tile in SMEM and TMA-stores it
+  int stage_slab;           // pair kernel: SMEM staging slab allocated (TMA or transpose epilogue)
   unsigned long long* trace;  // optional per-role cycle counters (LUTGPU_OH_TRACE), CTA 0 only
+  unsigned long long* tl;     // optional event timeline (LUTGPU_OH_TL=<file>), CTAs 0 and 1 (one pair)
   int sparse;               // 2:4-compressed one-hot A (tcgen05.mma.sp), else dense
   int stage_kb;             // pair kernel, sparse: 128-byte K blocks per A ring stage (1 or 2)
   int debug;                // ablation bits (LUTGPU_OH_DEBUG): 1 no epilogue math/stores, 2 no MMA,
@@ -577,6 +579,19 @@ __device__ __forceinline__ void commit_elect(uint64_t* bar, bool pair) {
 }
 
 // cycle accounting for the LUTGPU_OH_TRACE diagnostic (CTA 0, one lane per role)
+// Timeline probe (LUTGPU_OH_TL): %globaltimer stamps of pipeline events of the
+// first pair, indexed by global ring stage (generators / MMA) or unit (epilogue).
+constexpr int kTlN = 192, kTlEv = 20;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL(ev, idx)                                                                                  \
+  do {                                                                                               \
+    if (p.tl && blockIdx.x < 2 && (int)(idx) >= 0 && (int)(idx) < kTlN)                             \
+      p.tl[((int)blockIdx.x * kTlEv + (ev)) * kTlN + (int)(idx)] = gtime();                          \
+  } while (0)
 #define OH_T0(var) long long var = (p.trace && blockIdx.x == 0) ? clock64() : 0
 #define OH_ACC(slot, var) \
   do {                    \
@@ -1000,6 +1015,47 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Relaxed remote arrive / waits for the per-stage and per-unit handshakes.
+// No generic memory crosses the pair on these paths: the A stages and
+// accumulators live in TMEM and are ordered by tcgen05.wait::st/ld plus the
+// tcgen05 thread-sync fences around the arrive/wait.  A release.cluster arrive
+// compiles to MEMBAR.ALL.GPU (~1 us under the output stream) and an
+// acquire.cluster wait to CCTL.IVALL; the relaxed forms compile to neither.
+__device__ __forceinline__ void mbar_arrive_cluster_rlx(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ bool mbar_test_rlx(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.relaxed.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try_wait_rlx(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+// spin as in mbar_wait_crit (1: poll; else sleep-wait)
+__device__ __forceinline__ void mbar_wait_rlx(uint64_t* bar, uint32_t parity, int spin) {
+  if (spin == 1) {
+    while (!mbar_test_rlx(bar, parity)) {
+    }
+  } else {
+    while (!mbar_try_wait_rlx(bar, parity)) {
+    }
+  }
+}
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -1074,7 +1130,12 @@ __device__ __forceinline__ void mma_i8_ts_pair(uint32_t d_tmem, uint32_t a_tmem,
 
 
 
-template <int K, int DIGITS, int SP, int KB>
+// FAST: compile-time plain epilogue (int8 tables, one scale, no bias / act /
+// int32 output, TMA-store staging): the generic epilogue's runtime-selected
+// variants (bias, GELU, per-m-tile scales, digit recombination, direct
+// stores) inflate the kernel to ~200 KB of SASS and cost instruction-cache
+// misses and constant-bank reloads on every pass.
+template <int K, int DIGITS, int SP, int KB, int FAST = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     onehot_pair_kernel(const __grid_constant__ CUtensorMap codes_map, const __grid_constant__ CUtensorMap out_map,
                        const __grid_constant__ OneHotParams p) {
@@ -1095,7 +1156,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   const int MTU = NN / DIGITS;                             // real output columns per unit
   const int half_cols = MTU / 2;                           // real columns per epilogue half
   const int half_bytes = kRowsPerTile * half_cols * 4;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + (p.tma_out ? 2 * half_bytes : 0));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + (p.stage_slab ? 2 * half_bytes : 0));
   uint64_t* b_full = bars + 0;      // local: own half landed
   uint64_t* b_empty = bars + 1;     // multicast commit: MMAs done with B
   uint64_t* code_full = bars + 2;   // [2] local
@@ -1197,12 +1258,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     uint32_t as = 0, aph = 0;
     int ntile;
     int64_t rt;
+    int sig_g = 0;
     while (walk.next(ntile, rt)) {
       for (int st = 0; st < nst; ++st) {
-        mbar_wait_crit(&a_full[as], aph, p.spin == 3 ? 1 : p.spin);
+        if (p.debug & 256)
+          mbar_wait_crit(&a_full[as], aph, p.spin == 3 ? 1 : p.spin);
+        else
+          mbar_wait_rlx(&a_full[as], aph, p.spin == 3 ? 1 : p.spin);
         tc_fence_after();
         tc_fence_before();
-        if (lane == 0 && !(p.debug & 16)) mbar_arrive_cluster(a_full_l + as * 8);
+        if (lane == 0 && !(p.debug & 16)) {
+          if (p.debug & 256)
+            mbar_arrive_cluster(a_full_l + as * 8);
+          else
+            mbar_arrive_cluster_rlx(a_full_l + as * 8);
+        }
+        if (lane == 0) TL(3, sig_g);
+        ++sig_g;
         __syncwarp();
         if (++as == nas) {
           as = 0;
@@ -1227,6 +1299,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       bool has_next = look.next(nt_next, rt_next);
       const uint64_t b_desc0 = sw128_desc(b_smem);
       const uint64_t bstep = (uint64_t)((NH * kKB) >> 4);  // descriptor step of one 128-byte K block
+      int mma_g = 0, mma_unit = 0;
       while (has_next) {
         ntile = nt_next;
         rt = rt_next;
@@ -1241,8 +1314,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         }
         {
           OH_T0(t0);
-          mbar_wait_cluster(&acc_empty[acc], accphase ^ 1);
+          if (p.debug & 256)
+            mbar_wait_cluster(&acc_empty[acc], accphase ^ 1);
+          else
+            mbar_wait_rlx(&acc_empty[acc], accphase ^ 1, 0);
           OH_ACC(1, t0);
+          if (lane == 0) TL(6, mma_unit);
         }
         tc_fence_after();
         const uint32_t d_tmem = acc * NN;  // TMEM base is column 0: this CTA owns all 512 columns
@@ -1250,8 +1327,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int st = 0; st < nst; ++st) {
           {
             OH_T0(t0);
-            mbar_wait_crit(&a_full[as], aph, p.spin == 3 ? 1 : p.spin);
+            if (p.debug & 256)
+              mbar_wait_crit(&a_full[as], aph, p.spin == 3 ? 1 : p.spin);
+            else
+              mbar_wait_rlx(&a_full[as], aph, p.spin == 3 ? 1 : p.spin);
             OH_ACC(2, t0);
+            if (lane == 0) TL(4, mma_g);
           }
           tc_fence_after();
           if (!(p.debug & 2)) {
@@ -1273,11 +1354,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                              idesc, st != 0, 2 * st + 1 < p.nkb);
           }
           commit_elect(&a_empty[as], true);
+          if (lane == 0) TL(5, mma_g);
+          ++mma_g;
           if (++as == nas) {
             as = 0;
             aph ^= 1;
           }
         }
+        ++mma_unit;
         OH_ACC(3, t_unit);
         commit_elect(&acc_full[acc], true);
         if (!has_next || nt_next != ntile) commit_elect(b_empty, true);
@@ -1321,7 +1405,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           if (has1) c1.load(row_saddr, sw, 2 * st + 1);
           uint32_t w[32], we[8];
           build_sparse<K, 2>(c0, w, we);
-          mbar_wait_crit(&a_empty[as], aph ^ 1, p.spin == 3 ? 0 : p.spin);
+          if (lane == 0 && sub == 0) TL(0, my_g);
+          if (p.debug & 256)
+            mbar_wait_crit(&a_empty[as], aph ^ 1, p.spin == 3 ? 0 : p.spin);
+          else
+            mbar_wait_rlx(&a_empty[as], aph ^ 1, p.spin == 3 ? 0 : p.spin);
+          if (lane == 0 && sub == 0) TL(1, my_g);
           tc_fence_after();
           if (!(p.debug & 4)) {
             tmem_st32(lane_base + as * SC, w);
@@ -1338,6 +1427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&a_full[as]);
+          if (lane == 0 && sub == 0) TL(2, my_g);
           as += 2;
           if (as >= nas) {
             as -= nas;
@@ -1413,9 +1503,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const float scale0 = (DIGITS == 1 && p.scales) ? __ldg(p.scales) : 1.0f;
     const uint64_t scale2 = pk_f2(scale0, scale0);
     const bool etr = p.trace && blockIdx.x == 0 && warp == kEpiWarp0 && lane == 0;
+    const bool etl = warp == kEpiWarp0 && lane == 0;
+    int epi_unit = 0;
     while (walk.next(ntile, rt)) {
       long long e0 = etr ? clock64() : 0;
       mbar_wait(&acc_full[acc], accphase);
+      if (etl) TL(7, epi_unit);
       long long e1 = etr ? clock64() : 0;
       tc_fence_after();
       const int64_t row0 = rt * 2 * kRowsPerTile + rank * kRowsPerTile;
@@ -1433,8 +1526,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         long long e2 = etr ? clock64() : 0;
         long long e3 = e2;
         if (!(p.debug & 1) && p.tma_out) {
-          if (lane == 0) bulk_wait_read0();  // this warp's single staging slab: previous store fully read
+          if (lane == 0 && !(p.debug & 128)) bulk_wait_read0();  // this warp's single staging slab: previous store fully read
           __syncwarp();
+          if (etl) TL(11, epi_unit);
         }
         const uint32_t out_saddr = smem_u32(stage_out + hf * half_bytes) + row_in_tile * (ib * 4);
         for (int h2 = 0; h2 < npass; ++h2) {
@@ -1445,8 +1539,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           else
             tmem_ld16_lo(tb, v);
           tmem_ld_wait();
+          if (etl) TL(12 + 2 * h2, epi_unit);
         }
         if (h2 == npass - 1) {
+          if (etl) TL(8, epi_unit);
           // this warp's half of the accumulator is in registers: release it
           tc_fence_before();
           if (leader) {
@@ -1454,10 +1550,85 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             if (lane == 0) mbar_arrive(&acc_empty[acc]);
           } else {
             named_barrier_sync(4, 256);
-            if (elected) mbar_arrive_cluster(acc_empty_l + acc * 8);
+            if (elected) {
+              if (p.debug & 256)
+                mbar_arrive_cluster(acc_empty_l + acc * 8);
+              else
+                mbar_arrive_cluster_rlx(acc_empty_l + acc * 8);
+            }
           }
         }
         if (p.debug & 1) continue;
+        if constexpr (FAST == 2) {
+          // 32 columns of this row straight to HBM: four 256-bit stores, each a
+          // full 32-byte sector (no staging, no proxy fence, no TMA queue)
+          if (live) {
+            float* dst = p.out + row * p.M + m_base + hf * HC + h2 * 32;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float f[8];
+#pragma unroll
+              for (int j = 0; j < 8; j += 2) {
+                const uint64_t b = pk_f2(__int_as_float(0x4B400000 + (int)v[8 * q + j]),
+                                         __int_as_float(0x4B400000 + (int)v[8 * q + j + 1]));
+                up_f2(mul_f2(add_f2(b, kNegMagic2), scale2), f[j], f[j + 1]);
+              }
+              asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + 8 * q), "f"(f[0]),
+                           "f"(f[1]), "f"(f[2]), "f"(f[3]), "f"(f[4]), "f"(f[5]), "f"(f[6]), "f"(f[7])
+                           : "memory");
+            }
+          }
+          continue;
+        }
+        if constexpr (FAST == 3) {
+          // 32 columns of this row into this warp's 32-row slice of the swizzled
+          // slab, then read back transposed (8 lanes per row) and written as
+          // full 128-byte lines with coalesced 16-byte stores
+          const uint32_t dst = out_saddr + (uint32_t)(h2 * (kRowsPerTile * 32 * 4));
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float f0, f1, f2, f3;
+            const uint64_t b01 = pk_f2(__int_as_float(0x4B400000 + (int)v[4 * q]), __int_as_float(0x4B400000 + (int)v[4 * q + 1]));
+            const uint64_t b23 = pk_f2(__int_as_float(0x4B400000 + (int)v[4 * q + 2]), __int_as_float(0x4B400000 + (int)v[4 * q + 3]));
+            up_f2(mul_f2(add_f2(b01, kNegMagic2), scale2), f0, f1);
+            up_f2(mul_f2(add_f2(b23, kNegMagic2), scale2), f2, f3);
+            sts_v4(dst + (uint32_t)((q ^ swz) << 4), f0, f1, f2, f3);
+          }
+          __syncwarp();
+          const uint32_t slab = smem_u32(stage_out + hf * half_bytes) + (uint32_t)(h2 * (kRowsPerTile * 32 * 4)) +
+                                (uint32_t)(sub * 32 * 128);
+          const int c = lane & 7;
+          const int col = m_base + hf * HC + h2 * 32 + 4 * c;
+          const bool col_ok = col < p.M;  // M % 4 == 0: a 4-column chunk is wholly in or out
+          float* gbase = p.out + col;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = i * 4 + (lane >> 3);  // row inside this warp's slice
+            float4 x;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                         : "r"(slab + (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4))));
+            const int64_t grow = row0 + sub * 32 + r;
+            if (grow < p.n && col_ok) *reinterpret_cast<float4*>(gbase + grow * p.M) = x;
+          }
+          __syncwarp();
+          continue;
+        }
+        if constexpr (FAST == 1) {
+          // 32 columns of this row: exact int -> f32, times the table scale,
+          // into the 128B-swizzled staging slab (one 32-column box)
+          const uint32_t dst = out_saddr + (uint32_t)(((h2 * 32) >> ib_log2) * (kRowsPerTile * ib * 4));
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float f0, f1, f2, f3;
+            const uint64_t b01 = pk_f2(__int_as_float(0x4B400000 + (int)v[4 * q]), __int_as_float(0x4B400000 + (int)v[4 * q + 1]));
+            const uint64_t b23 = pk_f2(__int_as_float(0x4B400000 + (int)v[4 * q + 2]), __int_as_float(0x4B400000 + (int)v[4 * q + 3]));
+            up_f2(mul_f2(add_f2(b01, kNegMagic2), scale2), f0, f1);
+            up_f2(mul_f2(add_f2(b23, kNegMagic2), scale2), f2, f3);
+            sts_v4(dst + (uint32_t)((q ^ swz) << 4), f0, f1, f2, f3);
+          }
+          continue;
+        }
 #pragma unroll
         for (int c4 = 0; c4 < 2; ++c4) {
           const int cl = c4 * 16;   // column inside this pass (v index)
@@ -1558,18 +1729,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             }
           }
         }
+        if (etl) TL(13 + 2 * h2, epi_unit);
         }  // passes
         e3 = etr ? clock64() : 0;
+        if (etl) TL(9, epi_unit);
         if (p.tma_out && p.out && !(p.debug & 49)) {
           fence_proxy_async_smem();
           __syncwarp();
+          if (etl) TL(16, epi_unit);
           if (lane == 0) {
             for (int bx = 0; bx < half_cols / ib; ++bx)
               tma_store_2d(&out_map, stage_out + hf * half_bytes + bx * (kRowsPerTile * ib * 4) + sub * 32 * (ib * 4),
-                           m_base + hf * half_cols + bx * ib, (int32_t)(row0 + sub * 32));
+                           m_base + hf * half_cols + bx * ib,
+                           (int32_t)(((p.debug & 64) ? (row0 & 2047) : row0) + sub * 32));  // 64: L2-resident rows
             bulk_commit();
           }
         }
+        if (etl) TL(10, epi_unit);
+        ++epi_unit;
         // end of epilogue body
 
         if (etr) {
@@ -1761,9 +1938,23 @@ static int launch_onehot_k(const CUtensorMap& map, const CUtensorMap& omap, OneH
 template <int K, int DIGITS>
 static int launch_pair_k(const CUtensorMap& map, const CUtensorMap& omap, OneHotParams& p, size_t smem, int grid,
                          cudaStream_t stream) {
+  // plain int8 epilogue at NT = 64: FAST 1 = TMA-store staging, FAST 2 = direct 256-bit stores
+  const bool plain = DIGITS == 1 && p.sparse && p.stage_kb == 4 && p.out && !p.out_i32 && !p.bias && !p.act &&
+                     p.scale_mtile == 0 && p.out_hw == 0 && p.NT == 64 && !(p.debug & 512);
+  // LUTGPU_OH_EPI: 1 TMA-store staging, 2 direct 256-bit stores, 3 SMEM transpose + coalesced stores
+  int epi = 1;
+  if (const char* e = getenv("LUTGPU_OH_EPI")) epi = atoi(e);
+  p.stage_slab = p.tma_out;
+  if (!plain || !p.tma_out) epi = 0;  // the staging slab (sized for TMA) is needed by 1 and 3
+  if (epi == 2 && ((p.M % 128) != 0 || (reinterpret_cast<uintptr_t>(p.out) & 31) != 0)) epi = 1;
+  if (epi == 3 && ((p.M % 4) != 0 || (reinterpret_cast<uintptr_t>(p.out) & 15) != 0)) epi = 1;
+  if (epi == 2 || epi == 3) p.tma_out = 0;
   auto kern = !p.sparse            ? onehot_pair_kernel<K, DIGITS, 0, 2>
               : p.stage_kb == 1 ? onehot_pair_kernel<K, DIGITS, 1, 1>
-              : p.stage_kb == 4 ? onehot_pair_kernel<K, DIGITS, 1, 4>
+              : p.stage_kb == 4 ? (epi == 1   ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 1 : 0>
+                                   : epi == 2 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 2 : 0>
+                                   : epi == 3 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 3 : 0>
+                                              : onehot_pair_kernel<K, DIGITS, 1, 4>)
                                 : onehot_pair_kernel<K, DIGITS, 1, 2>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(onehot_pair)");
@@ -1898,6 +2089,32 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
     }
     const size_t smem = base_smem + (p.tma_out ? stage_bytes : 0);
     p.trace = nullptr;
+    p.tl = nullptr;
+    const char* tl_path = getenv("LUTGPU_OH_TL");
+    if (tl_path) {
+      cudaMalloc(&p.tl, 2 * kTlEv * kTlN * sizeof(unsigned long long));
+      cudaMemsetAsync(p.tl, 0, 2 * kTlEv * kTlN * sizeof(unsigned long long), stream);
+    }
+    struct TlDump {
+      unsigned long long* t;
+      cudaStream_t s;
+      const char* path;
+      ~TlDump() {
+        if (!t) return;
+        static unsigned long long h[2 * kTlEv * kTlN];
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h, t, sizeof(h), cudaMemcpyDeviceToHost);
+        if (FILE* f = fopen(path, "w")) {
+          fprintf(f, "cta,event,idx,ns\n");
+          for (int b = 0; b < 2; ++b)
+            for (int e = 0; e < kTlEv; ++e)
+              for (int i = 0; i < kTlN; ++i)
+                if (h[(b * kTlEv + e) * kTlN + i]) fprintf(f, "%d,%d,%d,%llu\n", b, e, i, h[(b * kTlEv + e) * kTlN + i]);
+          fclose(f);
+        }
+        cudaFree(t);
+      }
+    } tld{p.tl, stream, tl_path};
     if (getenv("LUTGPU_OH_TRACE")) {
       cudaMalloc(&p.trace, 16 * sizeof(unsigned long long));
       cudaMemsetAsync(p.trace, 0, 16 * sizeof(unsigned long long), stream);

@@ -364,3 +364,37 @@ def test_hash_encoder(L, golden):
     got = L.lut_layer_infer(a, layer, integer=False, encoder="hash")
     want = O.lut_matmul_ref(golden.arrays["hash_codes"], O.build_table(w, books))
     np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("n,m", [(3001, 4096), (1000, 640), (257, 200), (513, 132)])
+def test_tc_plain_epilogue_bitwise(L, n, m):
+    """The pair kernel's plain int8 epilogue (no bias / act, one scale: the
+    configs[4] bench call) == the CUDA-core int8 gather, bitwise, on partial
+    row tiles and on M not a multiple of the 128-column unit."""
+    import torch
+
+    from paper_2302_03213_b200._lib import load
+
+    lib = load()
+    c, k, v = 128, 16, 32
+    g = torch.Generator(device="cuda").manual_seed(n * 7 + m)
+    books = torch.randn((c, k, v), generator=g, device="cuda")
+    w = torch.randn((c * v, m), generator=g, device="cuda") * 0.02
+    layer = L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=books, weight=w, qat=True, gather="tensor")
+    assert layer.uses_tensor_cores(True)
+    a = torch.randn((n, c * v), generator=g, device="cuda")
+    cstride = int(lib.lut_code_stride(c))
+    codes = torch.empty((n, cstride), dtype=torch.uint8, device="cuda")
+    sp = torch.cuda.current_stream().cuda_stream
+    assert lib.lut_encode_f32(a.data_ptr(), n, c * v, layer.books_prep.data_ptr(), c, k, v, codes.data_ptr(), 8,
+                              cstride, None, sp) == 0
+    scales = layer.qtable.scales_tensor("cuda")
+    image = layer.onehot_image(True)
+    out_tc = torch.full((n, m), float("nan"), device="cuda")
+    out_cc = torch.empty((n, m), device="cuda")
+    assert lib.lut_gather_onehot(codes.data_ptr(), cstride, n, c, k, m, 1, image.data_ptr(), scales.data_ptr(), 0,
+                                 None, 0, out_tc.data_ptr(), None, 0, sp) == 0
+    assert lib.lut_gather_i8(codes.data_ptr(), 8, n, c, k, m, layer.qtable.q.data_ptr(), scales.data_ptr(), 0, None,
+                             0, out_cc.data_ptr(), None, 0, None, sp) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(out_tc, out_cc)
