@@ -151,7 +151,11 @@ __device__ __forceinline__ void store_code_group(uint8_t* dst, uint32_t w0, uint
   for (int i = 0; i < nbytes; ++i) dst[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
 }
 
-template <int V, int kEncWarps, int kRPL>
+// CHAIN = 1: one packed accumulator chain per (row, k) over raw a (the -2 is
+// applied once, d = fma(-2, a.p, |p|^2)): no per-element FMUL and no per-k
+// FADD2 merge; CHAIN = 0: |p|^2 seeded, two chains over -2a.  Both are sums of
+// V+1 rounded terms, inside the same error bound (TAU).
+template <int V, int kEncWarps, int kRPL, int CHAIN = 0>
 __global__ void __launch_bounds__((kEncWarps + 1) * 32, 1)
     encode_tma_kernel(const __grid_constant__ CUtensorMap tmap, const EncTmaParams p) {
   constexpr int kRowsPerPass = kEncWarps * 32;  // rows covered by one pass of all consumer lanes
@@ -251,8 +255,13 @@ __global__ void __launch_bounds__((kEncWarps + 1) * 32, 1)
             asq[r] = fmaf(x.y, x.y, asq[r]);
             asq[r] = fmaf(x.z, x.z, asq[r]);
             asq[r] = fmaf(x.w, x.w, asq[r]);
-            a2[r][2 * j + 0] = pack_f2(-2.0f * x.x, -2.0f * x.y);
-            a2[r][2 * j + 1] = pack_f2(-2.0f * x.z, -2.0f * x.w);
+            if constexpr (CHAIN == 1) {
+              a2[r][2 * j + 0] = pack_f2(x.x, x.y);
+              a2[r][2 * j + 1] = pack_f2(x.z, x.w);
+            } else {
+              a2[r][2 * j + 0] = pack_f2(-2.0f * x.x, -2.0f * x.y);
+              a2[r][2 * j + 1] = pack_f2(-2.0f * x.z, -2.0f * x.w);
+            }
           }
         }
         float best[kRPL], second[kRPL];
@@ -271,7 +280,7 @@ __global__ void __launch_bounds__((kEncWarps + 1) * 32, 1)
           uint64_t acc0[kRPL], acc1[kRPL];
 #pragma unroll
           for (int r = 0; r < kRPL; ++r) {
-            acc0[r] = pack_f2(pn, 0.0f);
+            acc0[r] = CHAIN == 1 ? 0ull : pack_f2(pn, 0.0f);
             acc1[r] = 0ull;
           }
 #pragma unroll
@@ -282,15 +291,26 @@ __global__ void __launch_bounds__((kEncWarps + 1) * 32, 1)
                          : "r"(cb_s + (uint32_t)((k * V + 4 * j) * 4)));
 #pragma unroll
             for (int r = 0; r < kRPL; ++r) {
-              acc0[r] = ffma2(a2[r][2 * j + 0], q01, acc0[r]);
-              acc1[r] = ffma2(a2[r][2 * j + 1], q23, acc1[r]);
+              if constexpr (CHAIN == 1) {
+                acc0[r] = ffma2(a2[r][2 * j + 0], q01, acc0[r]);
+                acc0[r] = ffma2(a2[r][2 * j + 1], q23, acc0[r]);
+              } else {
+                acc0[r] = ffma2(a2[r][2 * j + 0], q01, acc0[r]);
+                acc1[r] = ffma2(a2[r][2 * j + 1], q23, acc1[r]);
+              }
             }
           }
 #pragma unroll
           for (int r = 0; r < kRPL; ++r) {
             float lo, hi;
-            unpack_f2(fadd2(acc0[r], acc1[r]), lo, hi);
-            const float d = lo + hi;
+            float d;
+            if constexpr (CHAIN == 1) {
+              unpack_f2(acc0[r], lo, hi);
+              d = fmaf(-2.0f, lo + hi, pn);
+            } else {
+              unpack_f2(fadd2(acc0[r], acc1[r]), lo, hi);
+              d = lo + hi;
+            }
             second[r] = fminf(second[r], fmaxf(best[r], d));
             bi[r] = (d < best[r]) ? k : bi[r];
             best[r] = fminf(best[r], d);
@@ -798,10 +818,12 @@ static int launch_tma(const float* a, int64_t n, int d, const float* prep, int C
   const int64_t nunits = p.ntiles * p.ngroups;
   const int grid = (int)(nunits < nsm ? nunits : nsm);
   const size_t smem = (size_t)stages * stage_bytes + 2 * stages * sizeof(uint64_t) + 1024;
-  // rows per lane (LUTGPU_ENC_RPL = 2 or 4; default 4)
-  int rpl = 4;
-  if (const char* r = getenv("LUTGPU_ENC_RPL")) rpl = atoi(r) == 2 ? 2 : 4;
-  auto kern = rpl == 2 ? encode_tma_kernel<V, 8, 2> : encode_tma_kernel<V, 4, 4>;
+  // rows per lane (LUTGPU_ENC_RPL = 2 or 4; default 2), accumulator form (LUTGPU_ENC_CHAIN = 0 or 1)
+  int rpl = 2, chain = 1;
+  if (const char* r = getenv("LUTGPU_ENC_RPL")) rpl = atoi(r) == 4 ? 4 : 2;
+  if (const char* c = getenv("LUTGPU_ENC_CHAIN")) chain = atoi(c) == 0 ? 0 : 1;
+  auto kern = rpl == 2 ? (chain ? encode_tma_kernel<V, 8, 2, 1> : encode_tma_kernel<V, 8, 2, 0>)
+                       : (chain ? encode_tma_kernel<V, 4, 4, 1> : encode_tma_kernel<V, 4, 4, 0>);
   const int threads = rpl == 2 ? 9 * 32 : 5 * 32;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(encode_tma)");

@@ -66,6 +66,7 @@ struct OneHotParams {
   int spin;                 // 1: latency-critical waits poll instead of sleeping
   int tma_out;              // 1: epilogue stages the tile in SMEM and TMA-stores it
   int stage_slab;           // pair kernel: SMEM staging slab allocated (TMA or transpose epilogue)
+  int epi;                  // pair kernel epilogue variant (0 generic; plain int8: 1/4 TMA, 2 direct, 3 transpose)
   unsigned long long* trace;  // optional per-role cycle counters (LUTGPU_OH_TRACE), CTA 0 only
   unsigned long long* tl;     // optional event timeline (LUTGPU_OH_TL=<file>), CTAs 0 and 1 (one pair)
   int sparse;               // 2:4-compressed one-hot A (tcgen05.mma.sp), else dense
@@ -1525,7 +1526,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         const int npass = HC / pc;
         long long e2 = etr ? clock64() : 0;
         long long e3 = e2;
-        if (!(p.debug & 1) && p.tma_out) {
+        if (FAST == 4 && !(p.debug & 1)) {
+          // one thread per accumulator half stores the half's 128-row boxes: it waits
+          // until its previous stores have read the slab, then releases the half
+          if (sub == 0) {
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+            asm volatile("bar.arrive %0, 128;" ::"r"(5 + 2 * hf) : "memory");
+          } else {
+            named_barrier_sync(5 + 2 * hf, 128);
+          }
+        } else if (!(p.debug & 1) && p.tma_out) {
           if (lane == 0 && !(p.debug & 128)) bulk_wait_read0();  // this warp's single staging slab: previous store fully read
           __syncwarp();
           if (etl) TL(11, epi_unit);
@@ -1614,7 +1625,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           __syncwarp();
           continue;
         }
-        if constexpr (FAST == 1) {
+        if constexpr (FAST == 1 || FAST == 4) {
           // 32 columns of this row: exact int -> f32, times the table scale,
           // into the 128B-swizzled staging slab (one 32-column box)
           const uint32_t dst = out_saddr + (uint32_t)(((h2 * 32) >> ib_log2) * (kRowsPerTile * ib * 4));
@@ -1733,7 +1744,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         }  // passes
         e3 = etr ? clock64() : 0;
         if (etl) TL(9, epi_unit);
-        if (p.tma_out && p.out && !(p.debug & 49)) {
+        if (FAST == 4 && !(p.debug & 49)) {
+          fence_proxy_async_smem();
+          if (sub != 0) {
+            asm volatile("bar.arrive %0, 128;" ::"r"(6 + 2 * hf) : "memory");
+          } else {
+            named_barrier_sync(6 + 2 * hf, 128);
+            if (lane == 0) {
+              for (int bx = 0; bx < half_cols / 32; ++bx)
+                tma_store_2d(&out_map, stage_out + hf * half_bytes + bx * (kRowsPerTile * 32 * 4),
+                             m_base + hf * half_cols + bx * 32, (int32_t)row0);
+              bulk_commit();
+            }
+          }
+        } else if (p.tma_out && p.out && !(p.debug & 49)) {
           fence_proxy_async_smem();
           __syncwarp();
           if (etl) TL(16, epi_unit);
@@ -1938,22 +1962,13 @@ static int launch_onehot_k(const CUtensorMap& map, const CUtensorMap& omap, OneH
 template <int K, int DIGITS>
 static int launch_pair_k(const CUtensorMap& map, const CUtensorMap& omap, OneHotParams& p, size_t smem, int grid,
                          cudaStream_t stream) {
-  // plain int8 epilogue at NT = 64: FAST 1 = TMA-store staging, FAST 2 = direct 256-bit stores
-  const bool plain = DIGITS == 1 && p.sparse && p.stage_kb == 4 && p.out && !p.out_i32 && !p.bias && !p.act &&
-                     p.scale_mtile == 0 && p.out_hw == 0 && p.NT == 64 && !(p.debug & 512);
-  // LUTGPU_OH_EPI: 1 TMA-store staging, 2 direct 256-bit stores, 3 SMEM transpose + coalesced stores
-  int epi = 1;
-  if (const char* e = getenv("LUTGPU_OH_EPI")) epi = atoi(e);
-  p.stage_slab = p.tma_out;
-  if (!plain || !p.tma_out) epi = 0;  // the staging slab (sized for TMA) is needed by 1 and 3
-  if (epi == 2 && ((p.M % 128) != 0 || (reinterpret_cast<uintptr_t>(p.out) & 31) != 0)) epi = 1;
-  if (epi == 3 && ((p.M % 4) != 0 || (reinterpret_cast<uintptr_t>(p.out) & 15) != 0)) epi = 1;
-  if (epi == 2 || epi == 3) p.tma_out = 0;
+  const int epi = DIGITS == 1 ? p.epi : 0;
   auto kern = !p.sparse            ? onehot_pair_kernel<K, DIGITS, 0, 2>
               : p.stage_kb == 1 ? onehot_pair_kernel<K, DIGITS, 1, 1>
               : p.stage_kb == 4 ? (epi == 1   ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 1 : 0>
                                    : epi == 2 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 2 : 0>
                                    : epi == 3 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 3 : 0>
+                                   : epi == 4 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 4 : 0>
                                               : onehot_pair_kernel<K, DIGITS, 1, 4>)
                                 : onehot_pair_kernel<K, DIGITS, 1, 2>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -2082,12 +2097,32 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
     CUtensorMap omap;
     memset(&omap, 0, sizeof(omap));
     p.tma_out = 0;
+    p.stage_slab = 0;
+    p.epi = 0;
+    // plain int8 epilogue at NT = 64 (the configs[4] call): compile-time variant
+    // LUTGPU_OH_EPI: 4 per-half 128-row TMA stores (default), 1 per-warp 32-row TMA stores,
+    // 2 direct 256-bit stores, 3 SMEM transpose + coalesced stores
+    const bool plain = digits == 1 && p.sparse && p.stage_kb == 4 && out && !out_i32 && !bias && !act &&
+                       scale_mtile == 0 && out_hw == 0 && g.NT == 64 && !(p.debug & 512);
+    int epi = plain ? 4 : 0;
+    if (plain) {
+      if (const char* e = getenv("LUTGPU_OH_EPI")) epi = atoi(e);
+      if (epi < 0 || epi > 4) epi = 4;
+    }
     const char* e5 = getenv("LUTGPU_OH_TMAOUT");
     if (!(e5 && e5[0] == '0') && out && out_hw == 0 && (M % 4) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
         ib >= 4 && half_cols % ib == 0 && base_smem + stage_bytes <= max_smem_optin()) {
-      if (make_tmap_2d_f32_box(&omap, out, (uint64_t)M, (uint64_t)n, (uint32_t)ib, 32)) p.tma_out = 1;
+      if (make_tmap_2d_f32_box(&omap, out, (uint64_t)M, (uint64_t)n, (uint32_t)ib, epi == 4 ? kRowsPerTile : 32)) {
+        p.tma_out = 1;
+        p.stage_slab = 1;
+        p.epi = epi;
+      }
     }
-    const size_t smem = base_smem + (p.tma_out ? stage_bytes : 0);
+    if (p.epi == 2 && ((M % 128) != 0 || (reinterpret_cast<uintptr_t>(out) & 31) != 0)) p.epi = 1;
+    if (p.epi == 4 && ib != 32) p.epi = 1;
+    if (p.epi == 1 && make_tmap_2d_f32_box(&omap, out, (uint64_t)M, (uint64_t)n, (uint32_t)ib, 32) == false) p.epi = 0;
+    if (p.epi == 2 || p.epi == 3) p.tma_out = 0;
+    const size_t smem = base_smem + (p.stage_slab ? stage_bytes : 0);
     p.trace = nullptr;
     p.tl = nullptr;
     const char* tl_path = getenv("LUTGPU_OH_TL");

@@ -32,3 +32,23 @@ for c in (0, 1):
     per = [ys[i + 1][1] - ys[i][1] for i in range(5, len(ys) - 1)]
     print("epi cta%d: " % c + ", ".join(parts) + " | unit period %.0f" % st.median(per))
 print("M.accempty_ok(u) - L.epi.rel(u-2) %.0f" % d(0, 8, 0, 6, range(5, 150), 2))
+# per-unit MMA issuer breakdown: wait for acc_empty (epilogue-bound) vs the 4 a_full waits (generator-bound)
+nst = 4
+wa, wf, busy = [], [], []
+for u in range(6, 150):
+    try:
+        prev_issue = ev[(0, 5)][nst * u - 1]
+        ok = ev[(0, 6)][u]
+        wa.append(ok - prev_issue)
+        t = ok
+        for g in range(nst * u, nst * u + nst):
+            wf.append(ev[(0, 4)][g] - t)
+            busy.append(ev[(0, 5)][g] - ev[(0, 4)][g])
+            t = ev[(0, 5)][g]
+    except KeyError:
+        pass
+if wa:
+    print("MMA per unit: wait acc_empty %.0f ns, wait a_full %.0f ns (4 stages), issue %.0f ns (4 stages)"
+          % (st.mean(wa), 4 * st.mean(wf), 4 * st.mean(busy)))
+# epilogue release skew: peer vs leader
+print("epi release skew peer-leader %.0f ns" % d(0, 8, 1, 8, range(5, 150)))
