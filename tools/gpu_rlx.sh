@@ -1,14 +1,13 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out/rlx
-for e in 4 1; do LUTGPU_OH_EPI=$e timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/rlx/pytest.log 2>&1; echo "pytest rc=$? $(tail -1 gpurun_out/rlx/pytest.log)"; done
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/rlx/pytest.log 2>&1; echo "pytest rc=$? $(tail -1 gpurun_out/rlx/pytest.log)"
 run() {
   env "$@" timeout 200 python bench.py --no-cpu --no-e2e --steps 5 --warmup 2 > gpurun_out/rlx/b.json 2>gpurun_out/rlx/b.err
   python -c "import json;d=json.load(open('gpurun_out/rlx/b.json'));print('$*', d['roofline']['kernel_ms'])" 2>/dev/null || { echo "$* failed"; tail -2 gpurun_out/rlx/b.err; }
 }
 run X=0
+run LUTGPU_OH_DEBUG=2048
 run LUTGPU_OH_SPIN=0
-run LUTGPU_OH_SPIN=1
-run LUTGPU_OH_EPI=1
-run LUTGPU_OH_EPI=0
+run LUTGPU_OH_DEBUG=1
 LUTGPU_OH_TL=gpurun_out/rlx/tl.csv timeout 200 python bench.py --no-cpu --no-e2e --steps 1 --warmup 1 > /dev/null 2>&1
