@@ -73,7 +73,9 @@ LUT_API size_t lut_books_prep_bytes(int32_t c, int32_t k, int32_t v);
 /*
  * Precompute what encode needs from the codebooks, once per layer:
  * per codebook the centroids, ||p_k||^2 (f64-accurate, rounded to f32) and
- * max_k ||p_k||^2, packed for bulk copies.  Replaces the per-call
+ * max_k ||p_k||^2, packed for bulk copies; for V = 32, K = 16 also the
+ * centroids as a 128B-swizzled tf32 MMA operand tile and ||p_k|| rounded up
+ * (tensor-core candidate screening, csrc/encode_tc.cu).  Replaces the per-call
  * `p_norm = einsum(...)` of centroid_search_fast (kernels.py:72-74).
  */
 LUT_API int lut_prepare_books(const float* books, int32_t c, int32_t k, int32_t v,

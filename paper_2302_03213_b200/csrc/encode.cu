@@ -41,6 +41,23 @@ __global__ void prepare_books_kernel(const float* __restrict__ books, int C, int
   float* rec = prep + (size_t)c * S;
   const float* src = books + (size_t)c * K * V;
   for (int i = threadIdx.x; i < K * V; i += blockDim.x) rec[i] = src[i];
+  if (prep_has_tc(K, V)) {  // swizzled tf32 operand tile + |p_k| rounded up (encode_tc.cu)
+    float* tc = rec + prep_base(K, V);
+    for (int i = threadIdx.x; i < K * V; i += blockDim.x) {
+      const int k = i / V, j = i - (i / V) * V;
+      tc[k * 32 + 4 * ((j >> 2) ^ (k & 7)) + (j & 3)] = src[i];
+    }
+    if (threadIdx.x == 0) {  // 2^-7 max_k |p_k|, rounded up (screening half-width)
+      double mx = 0.0;
+      for (int k = 0; k < K; ++k) {
+        double s = 0.0;
+        for (int j = 0; j < V; ++j) s = fma((double)src[k * V + j], (double)src[k * V + j], s);
+        mx = fmax(mx, s);
+      }
+      tc[K * V] = __double2float_ru(sqrt(mx) * (1.0 + 1e-15) * 0.0078125);
+      for (int k = 1; k < K; ++k) tc[K * V + k] = 0.0f;
+    }
+  }
   __shared__ float smax[32];
   float local = 0.0f;
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
@@ -60,7 +77,7 @@ __global__ void prepare_books_kernel(const float* __restrict__ books, int C, int
     float m = 0.0f;
     for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) m = fmaxf(m, smax[w]);
     rec[K * V + K] = m;
-    for (int i = K * V + K + 1; i < S; ++i) rec[i] = 0.0f;
+    for (int i = K * V + K + 1; i < prep_base(K, V); ++i) rec[i] = 0.0f;
   }
 }
 
@@ -833,10 +850,19 @@ static int launch_tma(const float* a, int64_t n, int d, const float* prep, int C
   return LUT_OK;
 }
 
+int encode_dense_tc(const float* a, int64_t n, int d, const float* prep, int C, int K, int V, uint8_t* codes,
+                    int code_bits, int64_t code_stride, int* near_tie, cudaStream_t stream, bool* used);
+
 int encode_dense(const float* a, int64_t n, int d, const float* prep, int C, int K, int V, uint8_t* codes,
                  int code_bits, int64_t code_stride, int* near_tie, cudaStream_t stream, int force_generic) {
   if (n == 0 || C == 0) return LUT_OK;
   const bool aligned = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (reinterpret_cast<uintptr_t>(prep) & 15) == 0;
+  if (!force_generic && aligned && !(getenv("LUTGPU_ENC_TC") && getenv("LUTGPU_ENC_TC")[0] == '0')) {
+    bool used = false;
+    const int st = encode_dense_tc(a, n, d, prep, C, K, V, codes, code_bits, code_stride, near_tie, stream, &used);
+    if (st != LUT_OK) return st;
+    if (used) return LUT_OK;
+  }
   if (!force_generic && aligned && K <= 128 && n >= kTileRows / 2) {
     bool used = false;
     int st = LUT_OK;

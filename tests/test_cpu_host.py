@@ -30,7 +30,10 @@ def test_library_exports_every_header_symbol():
     assert set(declared) == set(_lib.SIGNATURES), "ctypes signature table out of sync with the header"
     h = _lib.load()
     assert h.lut_version() == 100
-    assert h.lut_books_prep_bytes(128, 16, 32) == 128 * ((16 * 32 + 16 + 1 + 3) // 4 * 4) * 4
+    # record: centroids, norms, max norm (padded to 4 floats); V=32, K=16 adds the
+    # swizzled tf32 operand tile and the rounded-up |p_k| of the screening encode
+    assert h.lut_books_prep_bytes(128, 16, 32) == 128 * ((16 * 32 + 16 + 1 + 3) // 4 * 4 + 16 * 32 + 16) * 4
+    assert h.lut_books_prep_bytes(48, 16, 16) == 48 * ((16 * 16 + 16 + 1 + 3) // 4 * 4) * 4
 
 
 def test_abi_rejects_bad_geometry_without_gpu():

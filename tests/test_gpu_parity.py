@@ -398,3 +398,30 @@ def test_tc_plain_epilogue_bitwise(L, n, m):
                              0, out_cc.data_ptr(), None, 0, None, sp) == 0
     torch.cuda.synchronize()
     assert torch.equal(out_tc, out_cc)
+
+
+def test_tc_screen_encode_exact(L):
+    """configs[1,3,4] encode shape (V=32, K=16) through the tensor-core screening
+    kernel: exact centroid hits, duplicated centroids (tie -> lowest k), scaled
+    near-duplicates and midpoints, plus random rows == encode_hard (oracle)."""
+    rng = O.make_rng(2024)
+    c, k, v, n = 8, 16, 32, 1000
+    books = rng.standard_normal((c, k, v)).astype(F32)
+    books[0, 9] = books[0, 3]                      # exact duplicate: lowest index wins
+    books[1, 15] = books[1, 0]
+    books[2, 7] = books[2, 6] * np.float32(1 + 2 ** -20)  # near duplicate
+    books[3] *= np.float32(1e3)                    # large magnitudes
+    books[4] *= np.float32(1e-3)                   # small magnitudes
+    a = rng.standard_normal((n, c * v)).astype(F32)
+    a[:, 3 * v:4 * v] *= np.float32(1e3)
+    a[:, 4 * v:5 * v] *= np.float32(1e-3)
+    for i in range(64):                            # exact hits and midpoints
+        cb = i % c
+        a[i, cb * v:(cb + 1) * v] = books[cb, i % k]
+        a[64 + i, cb * v:(cb + 1) * v] = (books[cb, i % k] + books[cb, (i + 5) % k]) * np.float32(0.5)
+    a[200:260, 0:v] = books[0, 3]                  # duplicated centroid hit
+    a[260:320, v:2 * v] = books[1, 0]
+    codes, ties = L.centroid_search_fast(a, books, return_near_ties=True)
+    np.testing.assert_array_equal(codes, O.encode_hard(a, books))
+    assert (codes[200:260, 0] == 3).all() and (codes[260:320, 1] == 0).all()
+    assert ties >= 120  # the duplicated-centroid hits are exact ties -> f64 re-decision

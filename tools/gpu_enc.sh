@@ -1,10 +1,10 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out/enc
-for cfg in "LUTGPU_ENC_CHAIN=2" "LUTGPU_ENC_CHAIN=1" "LUTGPU_ENC_CHAIN=2 LUTGPU_ENC_GEOM=4" "LUTGPU_ENC_CHAIN=2 LUTGPU_ENC_GEOM=12"; do
-  env $cfg timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/enc/pytest.log 2>&1; echo "$cfg pytest rc=$? $(tail -1 gpurun_out/enc/pytest.log)"
-  env $cfg timeout 300 python bench.py --no-cpu --no-e2e --steps 5 > gpurun_out/enc/b.json 2>/dev/null
-  python -c "import json;d=json.load(open('gpurun_out/enc/b.json'));print('$cfg', d['roofline']['kernel_ms'], d['near_ties'])"
-  env $cfg timeout 300 python bench.py --no-cpu --no-e2e --steps 3 --k 64 > gpurun_out/enc/b64.json 2>/dev/null
-  python -c "import json;d=json.load(open('gpurun_out/enc/b64.json'));print('K=64 $cfg', d['roofline']['kernel_ms'])"
+for g in 2 3 4; do
+  LUTGPU_ENC_TC_GROUPS=$g timeout 300 python -m pytest tests -m gpu -x -q -k "encode or ties or crit1 or cfg or large or screen" > gpurun_out/enc/pytest.log 2>&1; echo "groups=$g pytest rc=$? $(tail -1 gpurun_out/enc/pytest.log)"
+  LUTGPU_ENC_TC_GROUPS=$g timeout 120 python bench.py --no-cpu --no-e2e --steps 5 > gpurun_out/enc/b.json 2>gpurun_out/enc/b.err
+  python -c "import json;d=json.load(open('gpurun_out/enc/b.json'));print('groups=$g', d['roofline']['kernel_ms'], d['near_ties'])" || tail -3 gpurun_out/enc/b.err
 done
+
+
