@@ -67,6 +67,7 @@ struct OneHotParams {
   int tma_out;              // 1: epilogue stages the tile in SMEM and TMA-stores it
   int stage_slab;           // pair kernel: SMEM staging slab allocated (TMA or transpose epilogue)
   int epi;                  // pair kernel epilogue variant (0 generic; plain int8: 1/4 TMA, 2 direct, 3 transpose)
+  int watch;                // pair kernel: warp 18 polls the issuer's barriers and hands stages over (bar.sync)
   unsigned long long* trace;  // optional per-role cycle counters (LUTGPU_OH_TRACE), CTA 0 only
   unsigned long long* tl;     // optional event timeline (LUTGPU_OH_TL=<file>), CTAs 0 and 1 (one pair)
   int sparse;               // 2:4-compressed one-hot A (tcgen05.mma.sp), else dense
@@ -603,7 +604,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 // group of 4 consecutive warps covers all 128 rows whatever its first index.
 constexpr int kGenWarp0 = 2;   // warps 2..9: generators (parity = (warp-2)>>2)
 constexpr int kEpiWarp0 = 10;  // warps 10..13: epilogue (pair kernel: 10..17, one accumulator half each)
-constexpr int kPairThreads = 18 * 32;
+constexpr int kPairThreads = 19 * 32;  // + warp 18: the leader's barrier watcher
 constexpr int kGenWarps = 8;
 constexpr int kStageCols = 64;  // TMEM columns per A stage (2 K blocks x 128 B / 4 B)
 constexpr int kSparseStageCols = 40;  // 2:4 sparse stage: 32 compressed A + 8 metadata columns
@@ -1138,6 +1139,7 @@ constexpr int kPGen0 = 0;    // warps 0..7: one-hot generators (parity = warp >>
 constexpr int kPEpi0 = 8;    // warps 8..15: epilogue (accumulator half = (warp - 8) >> 2)
 constexpr int kPProd = 16;   // producer (B image, code tiles)
 constexpr int kPMma = 17;    // TMEM allocator + MMA issuer (leader) / peer signaler
+constexpr int kPWatch = 18;  // leader: barrier watcher for the MMA issuer
 
 // FAST: compile-time plain epilogue (int8 tables, one scale, no bias / act /
 // int32 output, TMA-store staging): the generic epilogue's runtime-selected
@@ -1259,6 +1261,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         }
       }
     }
+  } else if (warp == kPWatch) {
+    // ------------------------------------------------ barrier watcher (leader only)
+    // Polls acc_empty / a_full for the MMA issuer and hands each ready stage over
+    // through a named barrier: a poll loop in the issuing warp itself (a load
+    // round trip while the generators stream tcgen05.st into TMEM) drains the
+    // tensor pipe's shallow MMA queue (tools/sp_pair_bench.cu: 64 -> ~100 clk/MMA;
+    // with the hand-off 64 clk).
+    if (leader && p.watch) {
+      uint32_t as = 0, aph = 0;
+      int acc = 0;
+      uint32_t accphase = 0;
+      int ntile;
+      int64_t rt;
+      while (walk.next(ntile, rt)) {
+        mbar_wait_rlx(&acc_empty[acc], accphase ^ 1, 1);
+        for (int st = 0; st < nst; ++st) {
+          mbar_wait_rlx(&a_full[as], aph, 1);
+          named_barrier_sync(9, 64);
+          if (++as == nas) {
+            as = 0;
+            aph ^= 1;
+          }
+        }
+        if (++acc == p.n_acc) {
+          acc = 0;
+          accphase ^= 1;
+        }
+      }
+    }
   } else if (warp == kPMma && !leader) {
     // ------------------------------------------------ peer signaler
     // Forwards each ring stage the peer's generators completed to the leader's
@@ -1322,7 +1353,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           b_phase ^= 1;
           cur_ntile = ntile;
         }
-        {
+        if (!p.watch) {
           OH_T0(t0);
           if (p.debug & 256)
             mbar_wait_cluster(&acc_empty[acc], accphase ^ 1);
@@ -1335,7 +1366,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         const uint32_t d_tmem = acc * NN;  // TMEM base is column 0: this CTA owns all 512 columns
         OH_T0(t_unit);
         for (int st = 0; st < nst; ++st) {
-          if (!next_ready) {
+          if (p.watch) {
+            OH_T0(t0);
+            named_barrier_sync(9, 64);  // the watcher saw a_full (and, for st == 0, acc_empty)
+            OH_ACC(2, t0);
+          } else if (!next_ready) {
             OH_T0(t0);
             if (p.debug & 256)
               mbar_wait_crit(&a_full[as], aph, p.spin == 3 ? 1 : p.spin);
@@ -1354,7 +1389,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
               // Probe the next ring stage while these 4 MMAs are queued: a blocking
               // poll between stages (with the generators' tcgen05.st traffic on the
               // SM) otherwise leaves the tensor pipe idle for ~100-200 cycles.
-              if (!(p.debug & 2048)) {
+              if (!(p.debug & 2048) && !p.watch) {
                 const uint32_t as1 = as + 1 == nas ? 0 : as + 1;
                 next_ready = mbar_test_rlx(&a_full[as1], as + 1 == nas ? aph ^ 1 : aph);
               }
@@ -1506,7 +1541,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         cphase ^= 1;
       }
     }
-  } else if (warp >= kPEpi0) {
+  } else if (warp >= kPEpi0 && warp < kPEpi0 + 8) {
     // ------------------------------------------------ epilogue (both CTAs)
     const int sub = warp & 3;
     const int row_in_tile = sub * 32 + lane;
@@ -2081,6 +2116,7 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
       p.sparse = (e3 && e3[0] == '1') ? 0 : 1;
     }
     p.stage_kb = 4;  // 4 K blocks (8 sparse MMAs) per ring handshake
+    p.watch = !(getenv("LUTGPU_OH_WATCH") && getenv("LUTGPU_OH_WATCH")[0] == '0');
     {
       const char* e4 = getenv("LUTGPU_OH_KB");
       if (e4 && (e4[0] == '1' || e4[0] == '2' || e4[0] == '4')) p.stage_kb = e4[0] - '0';

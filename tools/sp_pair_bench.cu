@@ -34,6 +34,7 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int N, int iters, long long* out
   __shared__ __align__(8) uint64_t bar;
   __shared__ __align__(8) uint64_t bar2;
   __shared__ __align__(8) uint64_t bar3;
+  __shared__ uint32_t flag;
   uint32_t rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int warp = threadIdx.x >> 5;
@@ -42,6 +43,7 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int N, int iters, long long* out
     stop = 0;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 100000000;" ::"r"(smem_u32(&bar2)));
+    flag = 1;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar3)));
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar3)));
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -63,8 +65,16 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int N, int iters, long long* out
     long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
       const uint32_t a = 256 + (uint32_t)(i & 3) * 40;
-      if ((mode & 8) && !(i & 1)) {  // per 8 MMAs: poll a completed barrier (bar3, phase 0 done) + after_thread_sync
+      if ((mode & 256) && !(i & 1)) asm volatile("bar.sync 1, 64;" ::: "memory");  // hand-off from the watcher warp
+      if ((mode & 8) && ((mode & 64) ? !(i & 3) : !(i & 1))) {  // poll a completed barrier every 8 (or 16) MMAs
         uint32_t ok = 0;
+        if (mode & 128) {  // poll a plain SMEM flag word (LSU path) instead of an mbarrier
+          while (!ok) asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(ok) : "r"(smem_u32(&flag)) : "memory");
+        } else if (mode & 32)
+          while (!ok)
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0,1,0,p;\n\t}"
+                         : "=r"(ok) : "r"(smem_u32(&bar3)) : "memory");
+        else
         while (!ok)
           asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.relaxed.cluster.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0,1,0,p;\n\t}"
                        : "=r"(ok) : "r"(smem_u32(&bar3)) : "memory");
@@ -100,6 +110,15 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int N, int iters, long long* out
                    : "=r"(ok) : "r"(smem_u32(&bar)));
     if (threadIdx.x == 32) out[blockIdx.x] = clock64() - t0;
     stop = 1;
+  } else if (warp == 2 && (mode & 256) && (rank == 0 || G == 1)) {
+    // watcher: polls the (completed) barrier, then releases the issuer through a named barrier
+    for (int i = 0; i < iters; i += 2) {
+      uint32_t ok = 0;
+      while (!ok)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.relaxed.cluster.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0,1,0,p;\n\t}"
+                     : "=r"(ok) : "r"(smem_u32(&bar3)) : "memory");
+      asm volatile("bar.sync 1, 64;" ::: "memory");
+    }
   } else if (warp >= 4 && warp < 12 && (mode & 1)) {
     // generator-like: tcgen05.st x32 into A-ring columns of this warp's lane quarter
     const uint32_t a = t + ((uint32_t)((warp & 3) * 32) << 16) + 256 + (uint32_t)((warp >> 2) & 1) * 128;
@@ -174,6 +193,6 @@ static void run(int N, int blocks, int mode = 0) {
 }
 
 int main() {
-  for (int mode : {3, 11, 15, 27, 31, 9, 10}) run<2>(128, 148, mode);
+  for (int mode : {3, 256 + 3, 256 + 7, 15}) run<2>(128, 148, mode);
   return 0;
 }
