@@ -39,12 +39,12 @@ bool make_tmap_2d_u8(CUtensorMap* map, const void* base, uint64_t cols, uint64_t
                      bool swizzle128);
 
 // prepared codebook record (floats): [K*V centroids][K norms][pmax][pad to 4]
-// and, for the tensor-core encode shape (V = 32, K = 16), a tf32 operand tile
+// and, for the tensor-core encode shapes (V = 32, K = 16 or 64), a tf32 operand tile
 // of the centroids in the 128B-swizzled K-major layout (chunk j of centroid k
 // at k*32 + 4*(j ^ (k & 7)) floats) followed by 2^-7 max_k |p_k| rounded up
 // (and K-1 zero floats).
 __host__ __device__ inline int prep_base(int k, int v) { return ((k * v + k + 1) + 3) & ~3; }
-__host__ __device__ inline bool prep_has_tc(int k, int v) { return k == 16 && v == 32; }
+__host__ __device__ inline bool prep_has_tc(int k, int v) { return (k == 16 || k == 64) && v == 32; }
 __host__ __device__ inline int prep_stride(int k, int v) { return prep_base(k, v) + (prep_has_tc(k, v) ? k * v + k : 0); }
 
 // ---------------------------------------------------------------- device side

@@ -1,5 +1,5 @@
 // Nearest-centroid encode with tensor-core candidate screening (sm_100a),
-// for sub-vectors of V = 32 floats and K = 16 centroids (configs[1,3,4]).
+// for sub-vectors of V = 32 floats and K = 16 or 64 centroids (configs[1,3,4]).
 //
 // Semantics are those of encode.cu (indices identical to the reference's
 // encode_hard, lutkit/pq.py:171-174: literal f64 squared distances, ties ->
@@ -23,7 +23,7 @@
 //     re-decided from literal f64 differences over all K (encode_hard), and
 //     counted as a near tie.
 //
-// Kernel anatomy (one persistent CTA per SM, 2 + 4*GR warps, GR = 3 by default):
+// Kernel anatomy (one persistent CTA per SM, 2 + 4*GR warps, GR = 4 by default; NK = 16 or 64):
 //   warp 0     producer: per stage (one codebook of one 128-row tile) a TMA
 //              box of A (32 columns x 128 rows, 128B swizzle, 16 KB) plus the
 //              codebook's pre-swizzled tf32 B tile (2 KB) and norms by bulk copy.
@@ -40,13 +40,18 @@
 
 namespace lutgpu {
 
-constexpr int kTcStageBytes = 16384 + 2048 + 1024;  // A tile | B tile | norms (+pad to 1 KB)
-// GR consumer groups of 4 warps; the ring depth is a multiple of GR so that
-// every slot is always consumed by the same group
-template <int GR> struct TcGeom;
-template <> struct TcGeom<2> { static constexpr int stages = 10; };
-template <> struct TcGeom<3> { static constexpr int stages = 9; };
-template <> struct TcGeom<4> { static constexpr int stages = 8; };
+// Stage: A tile (16 KB) | B tile (NK x 128 B) | aux 1 KB: [NK |p|^2][pmax][pad] at 0,
+// 2^-7 max|p| at byte 512.  GR consumer groups of 4 warps; the ring depth is a
+// multiple of GR so that every slot is always consumed by the same group, and
+// stages x NK TMEM columns fit the 512.
+template <int NK> constexpr int tc_stage_bytes() { return 16384 + NK * 128 + 1024; }
+template <int GR, int NK> struct TcGeom;
+template <> struct TcGeom<2, 16> { static constexpr int stages = 10; };
+template <> struct TcGeom<3, 16> { static constexpr int stages = 9; };
+template <> struct TcGeom<4, 16> { static constexpr int stages = 8; };
+template <> struct TcGeom<2, 64> { static constexpr int stages = 8; };
+template <> struct TcGeom<3, 64> { static constexpr int stages = 6; };
+template <> struct TcGeom<4, 64> { static constexpr int stages = 8; };
 constexpr int kTcG = 16;                            // codebooks per unit (16 B of codes per row)
 
 struct EncTcParams {
@@ -71,9 +76,11 @@ __device__ __forceinline__ uint64_t tc_sw128_desc(uint32_t saddr) {
   return d;
 }
 
-// kind::tf32, D f32, A/B tf32 (K-major), M = 128, N = 16
-constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(16 >> 3) << 17) |
-                              ((uint32_t)(128 >> 4) << 24);
+// kind::tf32, D f32, A/B tf32 (K-major), M = 128, N = NK
+template <int NK>
+constexpr uint32_t tc_idesc() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NK >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
 
 __device__ __forceinline__ uint64_t f2pk(float lo, float hi) {
   uint64_t r;
@@ -89,10 +96,30 @@ __device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
   return d;
 }
 
-template <int GR>
+template <int NK> struct TcMask { using T = uint32_t; };
+template <> struct TcMask<64> { using T = uint64_t; };
+__device__ __forceinline__ int ffs_mask(uint32_t m) { return __ffs((int)m); }
+__device__ __forceinline__ int ffs_mask(uint64_t m) { return __ffsll((long long)m); }
+
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+
+template <int GR, int NK>
 __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
     encode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const EncTcParams p) {
-  constexpr int kTcStages = TcGeom<GR>::stages;
+  constexpr int kTcStages = TcGeom<GR, NK>::stages;
+  constexpr int kTcStageBytes = tc_stage_bytes<NK>();
+  constexpr int kAux = 16384 + NK * 128;             // aux offset inside a stage
+  constexpr uint32_t kTmemCols = NK == 16 ? 256 : 512;
+  static_assert(kTcStages * NK <= (int)kTmemCols, "TMEM slots");
+  using MaskT = typename TcMask<NK>::T;  // candidate set: one bit per centroid
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTcStages * kTcStageBytes);
@@ -112,7 +139,7 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(256)
+                 "r"(kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -135,11 +162,11 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * kTcStageBytes;
           const float* rec = p.prep + (size_t)c * p.S;
-          mbar_arrive_expect_tx(&full[stage], 16384 + 2048 + 80 + 64);
+          mbar_arrive_expect_tx(&full[stage], 16384 + NK * 128 + (NK + 4) * 4 + 64);
           tma_load_2d(st, &tmap, c * 32, (int32_t)(tile * 128), &full[stage]);
-          bulk_load(st + 16384, rec + prep_base(16, 32), 2048, &full[stage]);       // swizzled tf32 B tile
-          bulk_load(st + 18432, rec + 16 * 32, 80, &full[stage]);                   // |p_k|^2, pmax, pad
-          bulk_load(st + 18432 + 128, rec + prep_base(16, 32) + 512, 64, &full[stage]);  // 2^-7 max|p_k| (up)
+          bulk_load(st + 16384, rec + prep_base(NK, 32), NK * 128, &full[stage]);   // swizzled tf32 B tile
+          bulk_load(st + kAux, rec + NK * 32, (NK + 4) * 4, &full[stage]);           // |p_k|^2, pmax, pad
+          bulk_load(st + kAux + 512, rec + prep_base(NK, 32) + NK * 32, 64, &full[stage]);  // 2^-7 max|p_k| (up)
           if (++stage == kTcStages) {
             stage = 0;
             phase ^= 1;
@@ -160,7 +187,7 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
         const uint32_t sa = smem_u32(smem + stage * kTcStageBytes);
         const uint64_t adesc = tc_sw128_desc(sa);
         const uint64_t bdesc = tc_sw128_desc(sa + 16384);
-        const uint32_t d = tmem + (uint32_t)(stage * 16);
+        const uint32_t d = tmem + (uint32_t)(stage * NK);
         asm volatile(
             "{\n\t.reg .pred e, f, t;\n\t"
             "setp.ne.u32 f, %11, %11;\n\t"
@@ -171,7 +198,7 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
             "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %6, %7, %3, t;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %8, %9, %3, t;\n\t"
             "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t}" ::"r"(d),
-            "l"(adesc), "l"(bdesc), "r"(kTcIdesc), "l"(adesc + 2), "l"(bdesc + 2), "l"(adesc + 4), "l"(bdesc + 4),
+            "l"(adesc), "l"(bdesc), "r"(tc_idesc<NK>()), "l"(adesc + 2), "l"(bdesc + 2), "l"(adesc + 4), "l"(bdesc + 4),
             "l"(adesc + 6), "l"(bdesc + 6), "r"(smem_u32(&dfull[stage])), "r"(0u)
             : "memory");
         if (++stage == kTcStages) {
@@ -213,15 +240,9 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
         mbar_wait(&dfull[cur], cph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint8_t* st = smem + cur * kTcStageBytes;
+        const uint32_t dslot = lane_addr + (uint32_t)(cur * NK);
         uint32_t dv[16];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-            "%14, %15}, [%16];"
-            : "=r"(dv[0]), "=r"(dv[1]), "=r"(dv[2]), "=r"(dv[3]), "=r"(dv[4]), "=r"(dv[5]), "=r"(dv[6]),
-              "=r"(dv[7]), "=r"(dv[8]), "=r"(dv[9]), "=r"(dv[10]), "=r"(dv[11]), "=r"(dv[12]), "=r"(dv[13]),
-              "=r"(dv[14]), "=r"(dv[15])
-            : "r"(lane_addr + (uint32_t)(cur * 16))
-            : "memory");
+        tc_ld16(dslot, dv);
         // this row's sub-vector (fp32, from the swizzled A tile) and |a|^2
         const uint32_t arow = smem_u32(st) + (uint32_t)(r * 128);
         float a[32];
@@ -240,34 +261,57 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
         float sq_lo, sq_hi;
         f2up(sq, sq_lo, sq_hi);
         const float asq = sq_lo + sq_hi;
-        const float* aux = reinterpret_cast<const float*>(st + 18432);  // [16 |p|^2][pmax][pad] .. [2^-7 max|p|]
+        const float* aux = reinterpret_cast<const float*>(st + kAux);  // [NK |p|^2][pmax][pad] .. @512: 2^-7 max|p|
         const float* pn = aux;
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         // screening half-width, one per row: D = 2^-7 |a| max_k|p_k| + 2^-21 (|a|^2 + max_k |p_k|^2)
         // (|a| and max|p| rounded up); candidates: d~_k <= min_j d~_j + 2D (rounded up)
         const float al = __fmul_ru(__fsqrt_ru(asq), 1.0000002f);
-        const float hw = fmaf(al, aux[32], 4.7683716e-7f * (asq + aux[16]));
+        const float hw = fmaf(al, aux[128], 4.7683716e-7f * (asq + aux[NK]));
         float dt[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) dt[k] = fmaf(-2.0f, __uint_as_float(dv[k]), pn[k]);
         float mn = fminf(fminf(dt[0], dt[1]), fminf(dt[2], dt[3]));
 #pragma unroll
         for (int k = 4; k < 16; k += 4) mn = fminf(mn, fminf(fminf(dt[k], dt[k + 1]), fminf(dt[k + 2], dt[k + 3])));
-        const float thr = __fadd_ru(mn, 2.0f * hw);
-        uint32_t mask = 0;
+#pragma unroll 1
+        for (int kc = 16; kc < NK; kc += 16) {  // K = 64: the other 16-column chunks (minimum pass)
+          uint32_t dw[16];
+          tc_ld16(dslot + (uint32_t)kc, dw);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int k = 0; k < 16; ++k) mask |= (dt[k] <= thr) ? (1u << k) : 0u;
+          for (int k = 0; k < 16; k += 4) {
+            const float e0 = fmaf(-2.0f, __uint_as_float(dw[k]), pn[kc + k]);
+            const float e1 = fmaf(-2.0f, __uint_as_float(dw[k + 1]), pn[kc + k + 1]);
+            const float e2 = fmaf(-2.0f, __uint_as_float(dw[k + 2]), pn[kc + k + 2]);
+            const float e3 = fmaf(-2.0f, __uint_as_float(dw[k + 3]), pn[kc + k + 3]);
+            mn = fminf(mn, fminf(fminf(e0, e1), fminf(e2, e3)));
+          }
+        }
+        const float thr = __fadd_ru(mn, 2.0f * hw);
+        MaskT mask = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) mask |= (dt[k] <= thr) ? ((MaskT)1 << k) : (MaskT)0;
+#pragma unroll 1
+        for (int kc = 16; kc < NK; kc += 16) {  // K = 64: candidate pass (same fp32 expression)
+          uint32_t dw[16];
+          tc_ld16(dslot + (uint32_t)kc, dw);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            mask |= (fmaf(-2.0f, __uint_as_float(dw[k]), pn[kc + k]) <= thr) ? ((MaskT)1 << (kc + k)) : (MaskT)0;
+        }
         int code;
         if ((mask & (mask - 1)) == 0 && mask != 0) {
-          code = __ffs(mask) - 1;
+          code = ffs_mask(mask) - 1;
         } else {
           // refine the candidates in fp32 (encode.cu formulation) from the swizzled B tile
           const uint32_t btile = smem_u32(st + 16384);
           float best = FLT_MAX, second = FLT_MAX;
           int bi = 0;
-          uint32_t m = mask;
+          MaskT m = mask;
           while (m) {
-            const int k = __ffs(m) - 1;
+            const int k = ffs_mask(m) - 1;
             m &= m - 1;
             uint64_t acc = 0ull;
 #pragma unroll
@@ -287,14 +331,14 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
             best = fminf(best, dk);
           }
           code = bi;
-          if (!(second - best > tau_c * (asq + aux[16]))) {
+          if (!(second - best > tau_c * (asq + aux[NK]))) {
             // near tie (or NaN): literal f64 decision over all K (encode_hard)
             // over the candidates (every other k is provably farther), ascending k
             double bd = 0.0;
             int bk = -1;
-            uint32_t mm = mask ? mask : 0xFFFFu;  // NaN rows: all K, as encode_hard
+            MaskT mm = mask ? mask : (MaskT)(NK == 64 ? ~0ull : 0xFFFFull);  // NaN rows: all K, as encode_hard
             while (mm) {
-              const int k = __ffs(mm) - 1;
+              const int k = ffs_mask(mm) - 1;
               mm &= mm - 1;
               const float* crow = reinterpret_cast<const float*>(st + 16384 + k * 128);
               double s = 0.0;
@@ -335,7 +379,7 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
   }
 }
 
@@ -343,7 +387,7 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
 int encode_dense_tc(const float* a, int64_t n, int d, const float* prep, int C, int K, int V, uint8_t* codes,
                     int code_bits, int64_t code_stride, int* near_tie, cudaStream_t stream, bool* used) {
   *used = false;
-  if (V != 32 || K != 16 || code_bits != 8 || n < 128 || !prep_has_tc(K, V)) return LUT_OK;
+  if (V != 32 || (K != 16 && K != 64) || code_bits != 8 || n < 128 || !prep_has_tc(K, V)) return LUT_OK;
   if ((reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(prep) & 15) || (d % 4)) return LUT_OK;
   CUtensorMap tmap;
   if (!make_tmap_2d_f32(&tmap, a, (uint64_t)d, (uint64_t)n, 32, 128, true)) return LUT_OK;
@@ -360,12 +404,20 @@ int encode_dense_tc(const float* a, int64_t n, int d, const float* prep, int C, 
   p.near_tie = near_tie;
   const int nsm = num_sms();
   const int grid = (int)(p.nunits < nsm ? p.nunits : nsm);
-  int gr = 3;  // consumer groups (LUTGPU_ENC_TC_GROUPS = 2, 3 or 4)
-  if (const char* g = getenv("LUTGPU_ENC_TC_GROUPS")) gr = atoi(g) == 2 ? 2 : atoi(g) == 4 ? 4 : 3;
-  const int stages = gr == 2 ? TcGeom<2>::stages : gr == 3 ? TcGeom<3>::stages : TcGeom<4>::stages;
-  const size_t smem = (((size_t)stages * kTcStageBytes + 3 * stages * sizeof(uint64_t) + 16 + 127) & ~size_t(127)) + 4096 + 1024;
+  int gr = 4;  // consumer groups (LUTGPU_ENC_TC_GROUPS = 2, 3 or 4)
+  if (const char* g = getenv("LUTGPU_ENC_TC_GROUPS")) gr = atoi(g) == 2 ? 2 : atoi(g) == 3 ? 3 : 4;
+  int stages;
+  void (*kern)(const CUtensorMap, const EncTcParams);
+  if (K == 16) {
+    stages = gr == 2 ? TcGeom<2, 16>::stages : gr == 3 ? TcGeom<3, 16>::stages : TcGeom<4, 16>::stages;
+    kern = gr == 2 ? encode_tc_kernel<2, 16> : gr == 3 ? encode_tc_kernel<3, 16> : encode_tc_kernel<4, 16>;
+  } else {
+    stages = gr == 2 ? TcGeom<2, 64>::stages : gr == 3 ? TcGeom<3, 64>::stages : TcGeom<4, 64>::stages;
+    kern = gr == 2 ? encode_tc_kernel<2, 64> : gr == 3 ? encode_tc_kernel<3, 64> : encode_tc_kernel<4, 64>;
+  }
+  const size_t sb = K == 16 ? tc_stage_bytes<16>() : tc_stage_bytes<64>();
+  const size_t smem = (((size_t)stages * sb + 3 * stages * sizeof(uint64_t) + 16 + 127) & ~size_t(127)) + 4096 + 1024;
   if (smem > max_smem_optin()) return LUT_OK;
-  auto kern = gr == 2 ? encode_tc_kernel<2> : gr == 3 ? encode_tc_kernel<3> : encode_tc_kernel<4>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(encode_tc)");
   kern<<<grid, (2 + 4 * gr) * 32, smem, stream>>>(tmap, p);

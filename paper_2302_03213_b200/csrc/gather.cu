@@ -138,15 +138,20 @@ __global__ void __launch_bounds__(kGatherThreads)
   for (int mt = first_mt; mt < nmt; mt += mt_step) {
     const int m0 = mt * MT;
     __syncthreads();
+    const bool vec = (g.M & 3) == 0 && (reinterpret_cast<uintptr_t>(table) & 15) == 0;
     for (int i = threadIdx.x; i < g.C * g.K * LPR; i += blockDim.x) {
       const int ck = i / LPR, qq = i - ck * LPR;
       const int col = m0 + 4 * qq;
       const float* src = table + (int64_t)ck * g.M + col;
       float4 v;
-      v.x = col + 0 < g.M ? __ldg(src + 0) : 0.0f;
-      v.y = col + 1 < g.M ? __ldg(src + 1) : 0.0f;
-      v.z = col + 2 < g.M ? __ldg(src + 2) : 0.0f;
-      v.w = col + 3 < g.M ? __ldg(src + 3) : 0.0f;
+      if (vec && col + 3 < g.M) {
+        v = __ldg(reinterpret_cast<const float4*>(src));  // one 16-byte load per 4 columns
+      } else {
+        v.x = col + 0 < g.M ? __ldg(src + 0) : 0.0f;
+        v.y = col + 1 < g.M ? __ldg(src + 1) : 0.0f;
+        v.z = col + 2 < g.M ? __ldg(src + 2) : 0.0f;
+        v.w = col + 3 < g.M ? __ldg(src + 3) : 0.0f;
+      }
       tsm4[i] = v;
     }
     __syncthreads();

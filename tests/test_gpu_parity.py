@@ -400,12 +400,13 @@ def test_tc_plain_epilogue_bitwise(L, n, m):
     assert torch.equal(out_tc, out_cc)
 
 
-def test_tc_screen_encode_exact(L):
-    """configs[1,3,4] encode shape (V=32, K=16) through the tensor-core screening
-    kernel: exact centroid hits, duplicated centroids (tie -> lowest k), scaled
-    near-duplicates and midpoints, plus random rows == encode_hard (oracle)."""
-    rng = O.make_rng(2024)
-    c, k, v, n = 8, 16, 32, 1000
+@pytest.mark.parametrize("k", [16, 64])
+def test_tc_screen_encode_exact(L, k):
+    """configs[1,3,4] encode shapes (V=32, K=16 / 64) through the tensor-core
+    screening kernel: exact centroid hits, duplicated centroids (tie -> lowest k),
+    scaled near-duplicates and midpoints, plus random rows == encode_hard (oracle)."""
+    rng = O.make_rng(2024 + k)
+    c, v, n = 8, 32, 1000
     books = rng.standard_normal((c, k, v)).astype(F32)
     books[0, 9] = books[0, 3]                      # exact duplicate: lowest index wins
     books[1, 15] = books[1, 0]

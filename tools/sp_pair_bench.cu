@@ -64,7 +64,24 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int N, int iters, long long* out
     const uint64_t b = sw128_desc(smem_u32(sm + 32768));
     long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
-      const uint32_t a = 256 + (uint32_t)(i & 3) * 40;
+      uint32_t a = 256 + (uint32_t)(i & 3) * 40;
+      uint64_t bb = b;
+      uint32_t dd = t;
+      if (mode & 512) {
+        const int st = (i >> 1) & 3;                 // stage within the unit (2 asm blocks per stage)
+        const int half = i & 1;
+        const int unit = i >> 3;
+        a = 256 + (uint32_t)((i >> 1) % 3) * 80 + (uint32_t)half * 32;
+        bb = b + (uint64_t)(((4 * st + 2 * half) * 64 * 128) >> 4);
+        dd = t + (uint32_t)(unit & 1) * 128;
+        if (mode & 8192) dd = t;
+        if (mode & 16384) bb = b;
+        if (mode & 32768) a = 256 + (uint32_t)(i & 3) * 40;
+        if (mode & 4096) {  // A ring in columns 0..239, accumulators at 256 / 384
+          a -= 256;
+          dd += 256;
+        }
+      }
       if ((mode & 256) && !(i & 1)) asm volatile("bar.sync 1, 64;" ::: "memory");  // hand-off from the watcher warp
       if ((mode & 8) && ((mode & 64) ? !(i & 3) : !(i & 1))) {  // poll a completed barrier every 8 (or 16) MMAs
         uint32_t ok = 0;
@@ -81,7 +98,8 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int N, int iters, long long* out
         if (!(mode & 16)) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       }
       if constexpr (G == 2) {
-        asm volatile(SP_STAGE(2)::"r"(t), "r"(t + a), "l"(b), "r"(idesc), "r"((uint32_t)(i != 0)), "r"(t + a + 32)
+        asm volatile(SP_STAGE(2)::"r"(dd), "r"(t + a), "l"(bb), "r"(idesc), "r"((uint32_t)((i & 7) != 0)),
+                     "r"(t + a + 64 - 32 * (uint32_t)(i & 1) + 8 * (uint32_t)(i & 1))
                      : "memory");
         if ((mode & 4) && (i & 1)) {  // commit every 8 MMAs (multicast to both CTAs' barrier 2)
           asm volatile(
@@ -121,7 +139,7 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int N, int iters, long long* out
     }
   } else if (warp >= 4 && warp < 12 && (mode & 1)) {
     // generator-like: tcgen05.st x32 into A-ring columns of this warp's lane quarter
-    const uint32_t a = t + ((uint32_t)((warp & 3) * 32) << 16) + 256 + (uint32_t)((warp >> 2) & 1) * 128;
+    const uint32_t a = t + ((uint32_t)((warp & 3) * 32) << 16) + ((mode & 4096) ? 0u : 256u) + (uint32_t)((warp >> 2) & 1) * 128;
     long long n = 0;
     while (!stop && n < 200000) {
       asm volatile(
@@ -133,7 +151,7 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int N, int iters, long long* out
     }
   } else if (warp >= 12 && warp < 16 && (mode & 2)) {
     // epilogue-like: tcgen05.ld x32 from accumulator columns
-    const uint32_t a = t + ((uint32_t)((warp & 3) * 32) << 16) + 128;
+    const uint32_t a = t + ((uint32_t)((warp & 3) * 32) << 16) + ((mode & 4096) ? 384u : 128u);
     uint32_t s = 0;
     long long n = 0;
     while (!stop && n < 200000) {
@@ -175,9 +193,9 @@ static void run(int N, int blocks, int mode = 0) {
   cudaMalloc(&d, sizeof(long long) * blocks);
   cudaMemset(d, 0, sizeof(long long) * blocks);
   const int iters = 2048;
-  cudaFuncSetAttribute(bench<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  bench<G><<<blocks, 512, 100 * 1024>>>(N, iters, d, mode);
-  bench<G><<<blocks, 512, 100 * 1024>>>(N, iters, d, mode);
+  cudaFuncSetAttribute(bench<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  bench<G><<<blocks, 512, 200 * 1024>>>(N, iters, d, mode);
+  bench<G><<<blocks, 512, 200 * 1024>>>(N, iters, d, mode);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[256];
   cudaMemcpy(h, d, sizeof(long long) * blocks, cudaMemcpyDeviceToHost);
@@ -193,6 +211,6 @@ static void run(int N, int blocks, int mode = 0) {
 }
 
 int main() {
-  for (int mode : {3, 256 + 3, 256 + 7, 15}) run<2>(128, 148, mode);
+  for (int mode : {512 + 256 + 5, 8192 + 512 + 256 + 5, 16384 + 512 + 256 + 5, 32768 + 512 + 256 + 5, 8192 + 16384 + 512 + 256 + 5, 8192 + 32768 + 512 + 256 + 5, 16384 + 32768 + 512 + 256 + 5}) run<2>(128, 148, mode);
   return 0;
 }
