@@ -376,7 +376,16 @@ static int launch_tiled(void (*kern)(GatherArgs, const T*), int nmt, size_t smem
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGatherThreads, smem);
   if (per_sm < 1) per_sm = 1;
   const int slots = num_sms() * per_sm;
-  int grid = nmt >= slots ? slots : (slots / nmt) * nmt;
+  // CTAs per m-tile: each re-stages its m-tile's table slice, so with few rows cap
+  // the split at ~min_rows rows per CTA (LUTGPU_GATHER_MINROWS; 0 = no cap)
+  int64_t min_rows = 256;
+  if (const char* e = getenv("LUTGPU_GATHER_MINROWS")) min_rows = atoll(e);
+  int cpm = nmt >= slots ? 1 : slots / nmt;
+  if (min_rows > 0) {
+    const int64_t cap = (g.n + min_rows - 1) / min_rows;
+    if (cap < cpm) cpm = (int)(cap > 0 ? cap : 1);
+  }
+  int grid = nmt >= slots ? slots : cpm * nmt;
   kern<<<grid, kGatherThreads, smem, stream>>>(g, table);
   return LUT_OK;
 }
@@ -390,9 +399,17 @@ int gather_f32_strided(const uint8_t* codes, int code_bits, int64_t code_stride,
   const size_t budget = 200 * 1024;
   const size_t per_col = (size_t)C * K * sizeof(float);
   int MT = 0;
+  // m-tile width: the widest slice that fits; with few rows prefer narrower
+  // slices (more m-tiles, each CTA stages less) until the m-tiles fill the chip
+  int mt_cap = 64;
+  if (const char* e = getenv("LUTGPU_GATHER_MT")) mt_cap = atoi(e);
+  else if (n < 65536) {
+    const int floor_mt = n < 16384 ? 8 : 16;
+    while (mt_cap > floor_mt && (M + mt_cap - 1) / mt_cap < num_sms()) mt_cap /= 2;
+  }
   if (!force_generic && C > 0) {
     for (int cand : {64, 32, 16, 8, 4}) {
-      if (per_col * cand <= budget && (cand <= 4 || (M + 3) / 4 * 4 >= cand)) {
+      if (cand <= mt_cap && per_col * cand <= budget && (cand <= 4 || (M + 3) / 4 * 4 >= cand)) {
         MT = cand;
         break;
       }
