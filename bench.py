@@ -334,9 +334,13 @@ def main():
     # ---- e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        a_h = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
-        a_h.copy_(a)
-        o_h = torch.empty((n, m), dtype=torch.float32, pin_memory=True)
+        # one rank: the whole 2^20-row shard (17 GB in + 17 GB out, pinned); under
+        # torchrun every rank pins its own buffers, so cap them at 2^18 rows per rank
+        # (PCIe-bound either way: rows/s does not depend on the shard length)
+        ne = n if world == 1 else min(n, 1 << 18)
+        a_h = torch.empty((ne, d), dtype=torch.float32, pin_memory=True)
+        a_h.copy_(a[:ne])
+        o_h = torch.empty((ne, m), dtype=torch.float32, pin_memory=True)
         a_np, o_np = a_h.numpy(), o_h.numpy()
         L.lut_layer_infer(a_np[: 1 << 14], layer, integer=integer)  # warm the executor
         if world > 1:
@@ -355,8 +359,8 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         ok = bool(torch.equal(o_h[:4096].to(dev), out[:4096]))
-        e2e = {"value": rows_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * n * d,
-               "d2h_bytes_per_step": 4 * n * m, "steps": len(times), "matches_device_path": ok,
+        e2e = {"value": ne * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * ne * d,
+               "d2h_bytes_per_step": 4 * ne * m, "rows_per_gpu": ne, "steps": len(times), "matches_device_path": ok,
                "api": "paper_2302_03213_b200.lut_layer_infer(numpy pinned) -> lut_pipeline_run"}
         del a_h, o_h
 
