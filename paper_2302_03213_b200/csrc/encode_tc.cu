@@ -23,7 +23,7 @@
 //     re-decided from literal f64 differences over all K (encode_hard), and
 //     counted as a near tie.
 //
-// Kernel anatomy (one persistent CTA per SM, 2 + 4*GR warps, GR = 4 by default; NK = 16 or 64):
+// Kernel anatomy (one persistent CTA per SM, 2 + 4*GR warps, GR = 3 (K = 16) or 4 (K = 64); NK = K):
 //   warp 0     producer: per stage (one codebook of one 128-row tile) a TMA
 //              box of A (32 columns x 128 rows, 128B swizzle, 16 KB) plus the
 //              codebook's pre-swizzled tf32 B tile (2 KB) and norms by bulk copy.
@@ -218,25 +218,28 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
     const int sw = r & 7;
     const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
     const float tau_c = (4.0f * 32 + 16.0f) * 5.9604645e-8f;  // encode.cu TAU for V = 32
-    int stage = 0;
+    // this group's ring slots are grp, grp + GR, ... (GR divides the ring depth), visited in order
+    int stage = grp;
     uint32_t phase = 0;
-    int64_t sidx = 0;  // this CTA's ring stage counter
-    int ub = 0;        // code buffer of the current unit
-    for (int64_t u = blockIdx.x; u < p.nunits; u += gridDim.x) {
+    int umod = 0;  // (CTA ring stage index of the current unit's first stage) mod GR
+    int ub = 0;    // code buffer of the current unit
+    int lu = 0;    // this CTA's unit counter
+    for (int64_t u = blockIdx.x; u < p.nunits; u += gridDim.x, ++lu) {
       const int c0 = (int)(u % p.ngroups) * kTcG;
       const int c1 = min(p.C, c0 + kTcG);
       const int nst = c1 - c0;
       const int64_t tile = u / p.ngroups;
       const int64_t row = tile * 128 + r;
-      for (int cc = 0; cc < nst; ++cc, ++sidx) {
-        const int my = (int)(sidx % GR) == grp;
+      const int cc0 = (grp - umod + GR) % GR;
+      umod = (umod + nst) % GR;
+      for (int cc = cc0; cc < nst; cc += GR) {
         const int cur = stage;
         const uint32_t cph = phase;
-        if (++stage == kTcStages) {
-          stage = 0;
+        stage += GR;
+        if (stage >= kTcStages) {
+          stage -= kTcStages;
           phase ^= 1;
         }
-        if (!my) continue;
         mbar_wait(&dfull[cur], cph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint8_t* st = smem + cur * kTcStageBytes;
@@ -363,7 +366,7 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
       }
       // all groups' codes of this unit are in cbuf[ub]: one group writes them out
       named_barrier_sync(1, 128 * GR);
-      if (grp == (int)(u / gridDim.x) % GR && row < p.n) {
+      if (grp == lu % GR && row < p.n) {
         const uint8_t* src = cbuf + (ub * 128 + r) * 16;
         uint8_t* dst = p.codes + row * p.code_stride + c0;
         if (nst == 16 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
@@ -404,7 +407,7 @@ int encode_dense_tc(const float* a, int64_t n, int d, const float* prep, int C, 
   p.near_tie = near_tie;
   const int nsm = num_sms();
   const int grid = (int)(p.nunits < nsm ? p.nunits : nsm);
-  int gr = 4;  // consumer groups (LUTGPU_ENC_TC_GROUPS = 2, 3 or 4)
+  int gr = K == 16 ? 3 : 4;  // consumer groups (LUTGPU_ENC_TC_GROUPS = 2, 3 or 4)
   if (const char* g = getenv("LUTGPU_ENC_TC_GROUPS")) gr = atoi(g) == 2 ? 2 : atoi(g) == 3 ? 3 : 4;
   int stages;
   void (*kern)(const CUtensorMap, const EncTcParams);
