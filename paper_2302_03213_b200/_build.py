@@ -27,6 +27,10 @@ NVCC_FLAGS = [
 ]
 
 
+if os.environ.get("LUTGPU_BUILD_PROBES") == "1":  # compile in the pair-gather timeline / role probes
+    NVCC_FLAGS.append("-DLUTGPU_PROBES")
+
+
 def _nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
         if cand and (os.path.isabs(cand) and os.path.exists(cand) or not os.path.isabs(cand)):

@@ -589,6 +589,9 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// The probes compile in only with -DLUTGPU_PROBES (tools/build_probes.sh): their
+// parameter checks and clock reads otherwise sit on the MMA issuer's critical path.
+#ifdef LUTGPU_PROBES
 #define TL(ev, idx)                                                                                  \
   do {                                                                                               \
     if (p.tl && blockIdx.x < 2 && (int)(idx) >= 0 && (int)(idx) < kTlN)                             \
@@ -599,6 +602,17 @@ __device__ __forceinline__ unsigned long long gtime() {
   do {                    \
     if (p.trace && blockIdx.x == 0 && lane == 0) atomicAdd(p.trace + (slot), (unsigned long long)(clock64() - var)); \
   } while (0)
+#else
+#define TL(ev, idx) \
+  do {              \
+  } while (0)
+#define OH_T0(var) \
+  do {             \
+  } while (0)
+#define OH_ACC(slot, var) \
+  do {                    \
+  } while (0)
+#endif
 
 // Role warps.  A warp may only touch the TMEM lane quarter warp % 4, so each
 // group of 4 consecutive warps covers all 128 rows whatever its first index.
