@@ -426,3 +426,26 @@ def test_tc_screen_encode_exact(L, k):
     np.testing.assert_array_equal(codes, O.encode_hard(a, books))
     assert (codes[200:260, 0] == 3).all() and (codes[260:320, 1] == 0).all()
     assert ties >= 120  # the duplicated-centroid hits are exact ties -> f64 re-decision
+
+
+def test_tc_screen_encode_random_shapes(L):
+    """Tensor-core screening encode on random row counts / codebook counts (partial
+    128-row tiles, partial 16-codebook groups, K in {16, 64}) and value scales,
+    through both the numpy and the torch entry points == encode_hard."""
+    import torch
+
+    rng = O.make_rng(777)
+    for trial in range(12):
+        k = (16, 64)[trial % 2]
+        n = int(rng.integers(128, 2500))
+        c = int(rng.integers(1, 40))
+        scale = np.float32(10.0 ** rng.integers(-2, 3))
+        books = (rng.standard_normal((c, k, 32)) * scale).astype(F32)
+        a = (rng.standard_normal((n, c * 32)) * scale).astype(F32)
+        if trial % 3 == 0:  # rows sitting exactly on centroids
+            idx = rng.integers(0, k, size=(n, c))
+            a = books[np.arange(c)[None, :], idx].reshape(n, c * 32).copy()
+        want = O.encode_hard(a, books)
+        np.testing.assert_array_equal(L.centroid_search_fast(a, books), want, err_msg=f"trial {trial}")
+        got_t = L.centroid_search_fast(torch.from_numpy(a).cuda(), torch.from_numpy(books).cuda())
+        np.testing.assert_array_equal(got_t.cpu().numpy(), want, err_msg=f"trial {trial} (torch)")
