@@ -73,6 +73,7 @@ def load(path: str = LIB_PATH):
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("LUTGPU_LIB", path)  # A/B builds (tools/ab_lib.sh): another in-tree .so
     if not os.path.exists(path):
         raise ImportError(
             f"native library missing: {path} — run `python -m paper_2302_03213_b200._build` "

@@ -1288,10 +1288,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       uint32_t accphase = 0;
       int ntile;
       int64_t rt;
+      const int wspin = p.spin == 3 ? 1 : p.spin;
       while (walk.next(ntile, rt)) {
-        mbar_wait_rlx(&acc_empty[acc], accphase ^ 1, 1);
+        mbar_wait_rlx(&acc_empty[acc], accphase ^ 1, wspin);
         for (int st = 0; st < nst; ++st) {
-          mbar_wait_rlx(&a_full[as], aph, 1);
+          mbar_wait_rlx(&a_full[as], aph, wspin);
           named_barrier_sync(9, 64);
           if (++as == nas) {
             as = 0;
@@ -1355,6 +1356,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       const uint64_t bstep = (uint64_t)((NH * kKB) >> 4);  // descriptor step of one 128-byte K block
       int mma_g = 0, mma_unit = 0;
       bool next_ready = false;  // a_full of the stage at `as` already observed complete
+      // launch parameters the per-stage path tests, read once into registers
+      const int dbg = p.debug, spin = p.spin, nkb = p.nkb, n_acc = p.n_acc;
+      const bool watch = p.watch != 0;
       while (has_next) {
         ntile = nt_next;
         rt = rt_next;
@@ -1367,9 +1371,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           b_phase ^= 1;
           cur_ntile = ntile;
         }
-        if (!p.watch) {
+        if (!watch) {
           OH_T0(t0);
-          if (p.debug & 256)
+          if (dbg & 256)
             mbar_wait_cluster(&acc_empty[acc], accphase ^ 1);
           else
             mbar_wait_rlx(&acc_empty[acc], accphase ^ 1, 0);
@@ -1380,45 +1384,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         const uint32_t d_tmem = acc * NN;  // TMEM base is column 0: this CTA owns all 512 columns
         OH_T0(t_unit);
         for (int st = 0; st < nst; ++st) {
-          if (p.watch) {
+          if (watch) {
             OH_T0(t0);
             named_barrier_sync(9, 64);  // the watcher saw a_full (and, for st == 0, acc_empty)
             OH_ACC(2, t0);
           } else if (!next_ready) {
             OH_T0(t0);
-            if (p.debug & 256)
-              mbar_wait_crit(&a_full[as], aph, p.spin == 3 ? 1 : p.spin);
+            if (dbg & 256)
+              mbar_wait_crit(&a_full[as], aph, spin == 3 ? 1 : spin);
             else
-              mbar_wait_rlx(&a_full[as], aph, p.spin == 3 ? 1 : p.spin);
+              mbar_wait_rlx(&a_full[as], aph, spin == 3 ? 1 : spin);
             OH_ACC(2, t0);
           }
           if (lane == 0) TL(4, mma_g);
           tc_fence_after();
           next_ready = false;
-          if (!(p.debug & 2)) {
+          if (!(dbg & 2)) {
             if constexpr (SP && KB == 4) {
               const uint64_t bst = b_desc0 + (uint64_t)((4 * st * NH * kKB) >> 4);
               const uint32_t abase = a_col0 + as * SC;
-              issue_stage_sp<2>(d_tmem, abase, bst, bstep, idesc, st != 0, 4 * st + 1 < p.nkb, abase + 64);
+              issue_stage_sp<2>(d_tmem, abase, bst, bstep, idesc, st != 0, 4 * st + 1 < nkb, abase + 64);
               // Probe the next ring stage while these 4 MMAs are queued: a blocking
               // poll between stages (with the generators' tcgen05.st traffic on the
               // SM) otherwise leaves the tensor pipe idle for ~100-200 cycles.
-              if (!(p.debug & 2048) && !p.watch) {
+              if (!(dbg & 2048) && !watch) {
                 const uint32_t as1 = as + 1 == nas ? 0 : as + 1;
                 next_ready = mbar_test_rlx(&a_full[as1], as + 1 == nas ? aph ^ 1 : aph);
               }
-              if (4 * st + 2 < p.nkb)
-                issue_stage_sp<2>(d_tmem, abase + 32, bst + 2 * bstep, bstep, idesc, 1, 4 * st + 3 < p.nkb,
+              if (4 * st + 2 < nkb)
+                issue_stage_sp<2>(d_tmem, abase + 32, bst + 2 * bstep, bstep, idesc, 1, 4 * st + 3 < nkb,
                                   abase + 72);
             } else if constexpr (SP && KB == 1)
               issue_stage_sp1<2>(d_tmem, a_col0 + as * SC, b_desc0 + (uint64_t)((st * NH * kKB) >> 4), idesc, st != 0,
                                  a_col0 + as * SC + 16);
             else if constexpr (SP)
               issue_stage_sp<2>(d_tmem, a_col0 + as * SC, b_desc0 + (uint64_t)((2 * st * NH * kKB) >> 4), bstep,
-                                idesc, st != 0, 2 * st + 1 < p.nkb, a_col0 + as * SC + 32);
+                                idesc, st != 0, 2 * st + 1 < nkb, a_col0 + as * SC + 32);
             else
               issue_stage<2>(d_tmem, a_col0 + as * SC, b_desc0 + (uint64_t)((2 * st * NH * kKB) >> 4), bstep,
-                             idesc, st != 0, 2 * st + 1 < p.nkb);
+                             idesc, st != 0, 2 * st + 1 < nkb);
           }
           commit_elect(&a_empty[as], true);
           if (lane == 0) TL(5, mma_g);
@@ -1432,7 +1436,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         OH_ACC(3, t_unit);
         commit_elect(&acc_full[acc], true);
         if (!has_next || nt_next != ntile) commit_elect(b_empty, true);
-        if (++acc == p.n_acc) {
+        if (++acc == n_acc) {
           acc = 0;
           accphase ^= 1;
         }
