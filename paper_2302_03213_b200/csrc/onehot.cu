@@ -1640,6 +1640,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           }
         }
         if (p.debug & 1) continue;
+        if constexpr (FAST == 5) {
+          // fp32 tables, 4 digit planes, no bias / act: 8 real columns of this pass,
+          // exact int64 recombination, one f64 scale, into the swizzled staging slab
+          float f[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            long long t = 0;
+#pragma unroll
+            for (int dg = 3; dg >= 0; --dg) t = t * 256 + (long long)(int)v[j * 4 + dg];
+            const int m = m_base + (hf * HC + h2 * 32) / 4 + j;
+            const double sc = m < p.M ? __ldg(p.col_scale + m) : 0.0;
+            f[j] = (float)((double)t * sc);
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int ml = h2 * 8 + 4 * j;  // real column inside this half
+            const int box = ml >> ib_log2, within = ml & (ib - 1);
+            const int chunk = (within >> 2) ^ swz;
+            sts_v4(out_saddr + box * (kRowsPerTile * ib * 4) + (chunk << 4), f[4 * j], f[4 * j + 1], f[4 * j + 2],
+                   f[4 * j + 3]);
+          }
+          continue;
+        }
         if constexpr (FAST == 2) {
           // 32 columns of this row straight to HBM: four 256-bit stores, each a
           // full 32-byte sector (no staging, no proxy fence, no TMA queue)
@@ -2032,10 +2055,11 @@ static int launch_onehot_k(const CUtensorMap& map, const CUtensorMap& omap, OneH
 template <int K, int DIGITS>
 static int launch_pair_k(const CUtensorMap& map, const CUtensorMap& omap, OneHotParams& p, size_t smem, int grid,
                          cudaStream_t stream) {
-  const int epi = DIGITS == 1 ? p.epi : 0;
+  const int epi = DIGITS == 1 ? p.epi : (DIGITS == 4 && p.epi == 5) ? 5 : 0;
   auto kern = !p.sparse            ? onehot_pair_kernel<K, DIGITS, 0, 2>
               : p.stage_kb == 1 ? onehot_pair_kernel<K, DIGITS, 1, 1>
-              : p.stage_kb == 4 ? (epi == 1   ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 1 : 0>
+              : p.stage_kb == 4 ? (epi == 5   ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 4 ? 5 : 0>
+                                   : epi == 1 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 1 : 0>
                                    : epi == 2 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 2 : 0>
                                    : epi == 3 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 3 : 0>
                                    : epi == 4 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 4 : 0>
@@ -2180,6 +2204,10 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
       if (const char* e = getenv("LUTGPU_OH_EPI")) epi = atoi(e);
       if (epi < 0 || epi > 4) epi = 4;
     }
+    // plain fp32 (4 digit planes): compile-time recombination epilogue, per-warp TMA stores
+    if (digits == 4 && p.sparse && p.stage_kb == 4 && out && !out_i32 && !bias && !act && out_hw == 0 &&
+        g.NT == 64 && !(p.debug & 512) && !(getenv("LUTGPU_OH_EPI") && atoi(getenv("LUTGPU_OH_EPI")) == 0))
+      epi = 5;
     const char* e5 = getenv("LUTGPU_OH_TMAOUT");
     if (!(e5 && e5[0] == '0') && out && out_hw == 0 && (M % 4) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
         ib >= 4 && half_cols % ib == 0 && base_smem + stage_bytes <= max_smem_optin()) {

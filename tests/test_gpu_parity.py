@@ -398,6 +398,16 @@ def test_tc_plain_epilogue_bitwise(L, n, m):
                              0, out_cc.data_ptr(), None, 0, None, sp) == 0
     torch.cuda.synchronize()
     assert torch.equal(out_tc, out_cc)
+    # fp32 tables through 4 digit planes (plain recombination epilogue) vs the bitwise f32 gather
+    img_f = layer.onehot_image(False)
+    out_tf = torch.full((n, m), float("nan"), device="cuda")
+    out_cf = torch.empty((n, m), device="cuda")
+    assert lib.lut_gather_onehot(codes.data_ptr(), cstride, n, c, k, m, 4, img_f.data_ptr(), None, 0,
+                                 None, 0, out_tf.data_ptr(), None, 0, sp) == 0
+    assert lib.lut_gather_f32(codes.data_ptr(), 8, n, c, k, m, layer.table.data_ptr(), None, 0,
+                              out_cf.data_ptr(), 0, None, sp) == 0
+    torch.cuda.synchronize()
+    torch.testing.assert_close(out_tf, out_cf, rtol=1e-5, atol=1e-5)
 
 
 @pytest.mark.parametrize("k", [16, 64])
