@@ -459,3 +459,23 @@ def test_tc_screen_encode_random_shapes(L):
         np.testing.assert_array_equal(L.centroid_search_fast(a, books), want, err_msg=f"trial {trial}")
         got_t = L.centroid_search_fast(torch.from_numpy(a).cuda(), torch.from_numpy(books).cuda())
         np.testing.assert_array_equal(got_t.cpu().numpy(), want, err_msg=f"trial {trial} (torch)")
+
+
+@pytest.mark.parametrize("c,k,m", [(128, 16, 4096), (130, 16, 257), (64, 16, 130), (33, 64, 96), (17, 64, 200),
+                                   (72, 16, 1000)])
+def test_layer_configs4_family_vs_oracle(L, c, k, m):
+    """configs[4]-family layers (V = 32) through lut_layer_infer on both table
+    types, no bias (the plain epilogues): int8 output bytes-equal to the oracle's
+    lut_layer_infer, fp32 tensor-core output within rtol/atol 1e-5 of it."""
+    rng = O.make_rng(c * 1000 + k + m)
+    n, v = 700, 32
+    a = rng.standard_normal((n, c * v)).astype(F32)
+    books = rng.standard_normal((c, k, v)).astype(F32)
+    w = (rng.standard_normal((c * v, m)) / np.sqrt(c * v)).astype(F32)
+    layer = L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=books, weight=w, qat=True, gather="tensor")
+    table = O.build_table(w, books)
+    q, s = O.quantize_table(table)
+    got8 = L.lut_layer_infer(a, layer, integer=True)
+    assert got8.tobytes() == O.lut_layer_infer(a, books, q=q, scale=s).tobytes()
+    gotf = L.lut_layer_infer(a, layer, integer=False)
+    np.testing.assert_allclose(gotf, O.lut_layer_infer(a, books, table=table, integer=False), rtol=1e-5, atol=1e-5)
