@@ -1972,7 +1972,12 @@ static OneHotGeom onehot_geom(int C, int K, int M, int digits) {
   OneHotGeom g{};
   g.nkb = (C * K + kKB - 1) / kKB;
   const size_t budget = 144 * 1024;
-  int NT = 128;
+  // 64 B rows per CTA at most: the CTA-pair kernel (MMA N = 128 over two SMs) beats
+  // the single-CTA kernel at N = 128 even when the image would fit (configs[1]/[3]
+  // layers with C*K <= 1152: 79 -> 14 us for the FFN1 gather)
+  int NT = 64;
+  if (const char* e = getenv("LUTGPU_OH_SINGLE128"))
+    if (e[0] == '1') NT = 128;
   while (NT > 16 && (size_t)NT * g.nkb * kKB > budget) NT /= 2;
   // do not waste B rows on a small M
   while (NT > 16 && NT / 2 >= M * digits) NT /= 2;
