@@ -37,6 +37,21 @@ struct GatherArgs {
   int scale_mtile;
 };
 
+// Row base and column stride of the output: row-major (N, M) or NCHW (one 32-bit
+// division per row instead of a 64-bit one per element).
+__device__ __forceinline__ void out_row(const GatherArgs& g, int64_t row, int64_t& base, int64_t& cstride) {
+  if (g.out_hw > 0) {
+    const uint32_t hw = (uint32_t)g.out_hw;
+    const uint64_t b = row < 0xFFFFFFFFll ? (uint64_t)((uint32_t)row / hw) : (uint64_t)row / hw;
+    const int64_t pix = row - (int64_t)b * g.out_hw;
+    base = (int64_t)b * g.M * g.out_hw + pix;
+    cstride = g.out_hw;
+  } else {
+    base = row * g.M;
+    cstride = 1;
+  }
+}
+
 __device__ __forceinline__ int64_t out_index(const GatherArgs& g, int64_t row, int col) {
   if (g.out_hw > 0) {
     const int64_t b = row / g.out_hw;
@@ -211,9 +226,11 @@ __global__ void __launch_bounds__(kGatherThreads)
             (reinterpret_cast<uintptr_t>(g.out) & 15) == 0) {
           *reinterpret_cast<float4*>(g.out + rows[r] * g.M + col0) = make_float4(v[0], v[1], v[2], v[3]);
         } else {
+          int64_t base, cs;
+          out_row(g, rows[r], base, cs);
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (col0 + e < g.M) g.out[out_index(g, rows[r], col0 + e)] = v[e];
+            if (col0 + e < g.M) g.out[base + (int64_t)(col0 + e) * cs] = v[e];
         }
       }
     }
@@ -321,11 +338,13 @@ __global__ void __launch_bounds__(kGatherThreads)
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
         if (rows[r] >= g.n) continue;
+        int64_t base, cs;
+        out_row(g, rows[r], base, cs);
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int col = col0 + e;
           if (col >= g.M) continue;
-          const int64_t o = out_index(g, rows[r], col);
+          const int64_t o = base + (int64_t)col * cs;
           if (g.out_i32) g.out_i32[o] = tot[r][e];
           if (g.out) {
             float f = __fmul_rn(__int2float_rn(tot[r][e]), scale_of(g, col));
