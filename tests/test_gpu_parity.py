@@ -479,3 +479,24 @@ def test_layer_configs4_family_vs_oracle(L, c, k, m):
     assert got8.tobytes() == O.lut_layer_infer(a, books, q=q, scale=s).tobytes()
     gotf = L.lut_layer_infer(a, layer, integer=False)
     np.testing.assert_allclose(gotf, O.lut_layer_infer(a, books, table=table, integer=False), rtol=1e-5, atol=1e-5)
+
+
+def test_conv_int8_tensor_nchw(L):
+    """A 3x3 LUT conv with int8 tables through the tensor-core gather writing NCHW
+    directly (out_hw > 0) == the oracle on the im2col matrix, bitwise."""
+    import torch
+
+    rng = O.make_rng(404)
+    bsz, cin, hh, ww, cout = 3, 16, 10, 12, 48
+    x = np.abs(rng.standard_normal((bsz, cin, hh, ww))).astype(F32)
+    books = np.abs(rng.standard_normal((cin, 16, 9))).astype(F32)
+    wconv = (rng.standard_normal((cin * 9, cout)) * 0.1).astype(F32)
+    layer = L.LutLayer(cfg=L.PqConfig(v=9, k=16), books=books, weight=wconv, qat=True, gather="tensor")
+    conv = L.LutConv(cin, 3, 1, 1, layer)
+    y, _ = conv.forward(x, integer=True)
+    cols = O.im2col(x, 3, 3, 1, 1)
+    table = O.build_table(wconv, books)
+    q, s = O.quantize_table(table)
+    want = O.lut_layer_infer(cols, books, q=q, scale=s).reshape(bsz, hh, ww, cout).transpose(0, 3, 1, 2)
+    got = y.cpu().numpy() if isinstance(y, torch.Tensor) else np.asarray(y)
+    assert got.tobytes() == np.ascontiguousarray(want).tobytes()
