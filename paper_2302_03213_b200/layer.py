@@ -8,6 +8,7 @@ object with the same attributes) is converted once and cached."""
 from __future__ import annotations
 
 import ctypes as C
+import os
 import weakref
 
 import numpy as np
@@ -22,7 +23,7 @@ from .quant import LookupTableI8, dequantize, quantize_table
 
 F32 = np.float32
 PIPELINE_MIN_BYTES = 32 << 20   # numpy inputs above this stream through the native executor
-PIPELINE_CHUNK_BYTES = 256 << 20
+PIPELINE_CHUNK_BYTES = int(os.environ.get("LUTGPU_PIPELINE_CHUNK_MB", "256")) << 20  # per input chunk
 
 
 class LutLayer:
