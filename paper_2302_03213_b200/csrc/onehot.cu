@@ -14,23 +14,30 @@
 // far inside the fp32 contract (rtol/atol 1e-5, BASELINE north star); the
 // bitwise ascending-c fp32 path remains in gather.cu.
 //
-// Kernel anatomy (single-CTA variant: one persistent CTA per SM, 14 warps):
-//   warp 0      producer: bulk-copies the prepared B image of the current
-//               n-tile (resident in SMEM, reloaded only when the n-tile
-//               changes) and TMA-loads 128-row code tiles (128B swizzle).
-//   warp 1      TMEM allocator + MMA issuer (one elected lane):
-//               tcgen05.mma.cta_group::1.kind::i8 (or .sp), A from TMEM, B from SMEM.
-//   warps 2-9   one-hot generators: thread = row = TMEM lane (quarter warp%4);
-//               builds the row's (2:4-compressed) one-hot bytes in registers
-//               and tcgen05.st's them into the A ring in TMEM (the A operand
-//               never touches shared memory).
-//   warps 10-13 epilogue: tcgen05.ld the int32 accumulator (double
-//               buffered in TMEM), scale (+digit recombination), bias, act,
-//               swizzled SMEM staging + TMA store.
-// The CTA-pair kernel (below) is the configs[4] fast path.
-// Work = (n-tile, 128-row tile) units, walked in row bands so every CTA works
-// near the same rows (codes stay in L2) while each CTA keeps one n-tile's B
-// image for many consecutive row tiles.
+// The A operand is 2:4 sparse by construction (one non-zero per K positions):
+// tcgen05.mma.sp with the compressed one-hot and its metadata in TMEM.
+//
+// onehot_pair_kernel (the default engine): a CTA pair (cluster of 2, cta_group::2)
+// computes 256 rows x 128 columns per unit; each SM keeps 64 columns of the B
+// image resident in SMEM (the pair's half) and generates the one-hot of its
+// own 128 rows straight into TMEM.  19 warps per CTA:
+//   warps 0-7   generators: thread = row = TMEM lane (lane quarter warp % 4); two
+//               parity groups build alternate ring stages (4 K blocks = 8 MMAs)
+//               in registers and tcgen05.st them into a 3-deep A ring.
+//   warps 8-15  epilogue: tcgen05.ld the double-buffered int32 accumulator;
+//               compile-time plain variants (FAST 1-5) for the scale-only int8 and
+//               fp32-digit calls, a runtime-generic one for bias / act / per-m-tile
+//               scales / NCHW / int32 output; swizzled SMEM staging + TMA store.
+//   warp 16     producer: B image bulk copies (once per n-tile), code tiles by TMA.
+//   warp 17     TMEM allocator; leader: MMA issuer (one elected lane, A from TMEM,
+//               B from SMEM); peer: forwards its generators' stage completions.
+//   warp 18     leader: barrier watcher — polls acc_empty / a_full and hands each
+//               ready stage to the issuer through a named barrier.
+// onehot_gemm_kernel: the single-CTA variant (14 warps, MMA N = NT) for shapes the
+// pair cannot take (an fp32 B image of fewer than 32 columns per CTA).
+// Work = (n-tile, row tile) units, walked in row bands so every CTA works near the
+// same rows (codes stay in L2) while each keeps one n-tile's B image for many
+// consecutive row tiles.
 
 #include "common.cuh"
 
