@@ -21,6 +21,14 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
 #define SP_G(G, AOFF, BOFF, EOFF)                                                       \
   "add.u32 ta, %1, " #AOFF ";\n\tadd.u64 tb, %2, " #BOFF ";\n\tadd.u32 te, %5, " #EOFF ";\n\t" \
   "@e tcgen05.mma.sp.cta_group::" #G ".kind::i8 [%0], [ta], tb, [te], %3, p0;\n\t"
+#define SP_GS(G, AOFF, BOFF, EOFF)                                                      \
+  "add.u64 tas, %6, " #AOFF ";\n\tadd.u64 tb, %2, " #BOFF ";\n\tadd.u32 te, %5, " #EOFF ";\n\t" \
+  "@e tcgen05.mma.sp.cta_group::" #G ".kind::i8 [%0], tas, tb, [te], %3, p0;\n\t"
+// A operand from SMEM (descriptor %6) instead of TMEM; metadata still in TMEM
+#define SP_STAGE_AS(G)                                                                    \
+  "{\n\t.reg .pred e, p0;\n\t.reg .b32 te;\n\t.reg .b64 tb, tas;\n\t"                 \
+  "elect.sync _|e, 0xffffffff;\n\tsetp.ne.u32 p0, %4, 0;\n\t"                          \
+  SP_GS(G, 0, 0, 0) SP_GS(G, 2, 4, 2) SP_GS(G, 4, 8, 4) SP_GS(G, 6, 12, 6) "}"
 #define SP_STAGE(G)                                                                       \
   "{\n\t.reg .pred e, p0;\n\t.reg .b32 ta, te;\n\t.reg .b64 tb;\n\t"                     \
   "elect.sync _|e, 0xffffffff;\n\tsetp.ne.u32 p0, %4, 0;\n\t"                          \
@@ -98,6 +106,19 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int N, int iters, long long* out
         if (!(mode & 16)) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       }
       if constexpr (G == 2) {
+        if ((mode & 65536) && !(i & 1)) {  // stage A (80 cols) from SMEM into TMEM with 10 tcgen05.cp 128x256b
+          const uint64_t src = sw128_desc(smem_u32(sm) + (uint32_t)((i >> 1) & 1) * 40960);
+#pragma unroll
+          for (int j = 0; j < 10; ++j)
+            asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                         "@e tcgen05.cp.cta_group::2.128x256b [%0], %1;\n\t}" ::"r"(t + a + 8 * j),
+                         "l"(src + (uint64_t)((j * 4096) >> 4)) : "memory");
+        }
+        if (mode & 262144)
+          asm volatile(SP_STAGE_AS(2)::"r"(dd), "r"(t + a), "l"(bb), "r"(idesc), "r"((uint32_t)((i & 7) != 0)),
+                       "r"(t + a + 64 - 32 * (uint32_t)(i & 1) + 8 * (uint32_t)(i & 1)),
+                       "l"(sw128_desc(smem_u32(sm) + (uint32_t)(i & 3) * 8192)) : "memory");
+        else
         asm volatile(SP_STAGE(2)::"r"(dd), "r"(t + a), "l"(bb), "r"(idesc), "r"((uint32_t)((i & 7) != 0)),
                      "r"(t + a + 64 - 32 * (uint32_t)(i & 1) + 8 * (uint32_t)(i & 1))
                      : "memory");
@@ -141,6 +162,16 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int N, int iters, long long* out
     // generator-like: tcgen05.st x32 into A-ring columns of this warp's lane quarter
     const uint32_t a = t + ((uint32_t)((warp & 3) * 32) << 16) + ((mode & 4096) ? 0u : 256u) + (uint32_t)((warp >> 2) & 1) * 128;
     long long n = 0;
+    if (mode & 131072) {  // same bytes as STS into the SMEM A image (4 KB per warp iteration)
+      const uint32_t base = smem_u32(sm) + (uint32_t)(warp - 4) * 4096 + (threadIdx.x & 31) * 16;
+      while (!stop && n < 200000) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + j * 512), "r"((uint32_t)n) : "memory");
+        asm volatile("bar.sync %0, 32;" ::"r"(2 + warp - 4) : "memory");
+        ++n;
+      }
+    } else
     while (!stop && n < 200000) {
       asm volatile(
           "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
@@ -211,6 +242,13 @@ static void run(int N, int blocks, int mode = 0) {
 }
 
 int main() {
-  for (int mode : {512 + 256 + 5, 8192 + 512 + 256 + 5, 16384 + 512 + 256 + 5, 32768 + 512 + 256 + 5, 8192 + 16384 + 512 + 256 + 5, 8192 + 32768 + 512 + 256 + 5, 16384 + 32768 + 512 + 256 + 5}) run<2>(128, 148, mode);
+  // 772: no generators (MMA-bound floor); 773: tcgen05.st generators (the shipped layout);
+  // +65536: A staged SMEM->TMEM by tcgen05.cp; +131072: generators write SMEM (STS) instead;
+  // +262144: A read by the MMA straight from SMEM (descriptor), metadata still in TMEM.
+  for (int mode : {0, 4, 260, 516, 772 + 8192, 772 + 16384, 772 + 32768, 772 + 8192 + 16384 + 32768, 772, 773, 772 + 65536, 773 + 65536, 773 + 131072, 773 + 65536 + 131072, 772 + 262144,
+                   773 + 262144 + 131072, 775 + 65536 + 131072, 775 + 262144 + 131072, 775})
+    run<2>(128, 148, mode);
+  for (int n : {128, 256})  // one accumulator at column 256, A ring at 0..239
+    for (int mode : {4, 772 + 4096 + 8192, 773 + 4096 + 8192, 775 + 4096 + 8192}) run<2>(n, 148, mode);
   return 0;
 }
