@@ -25,9 +25,10 @@
 //               parity groups build alternate ring stages (4 K blocks = 8 MMAs)
 //               in registers and tcgen05.st them into a 3-deep A ring.
 //   warps 8-15  epilogue: tcgen05.ld the double-buffered int32 accumulator;
-//               compile-time plain variants (FAST 1-5) for the scale-only int8 and
-//               fp32-digit calls, a runtime-generic one for bias / act / per-m-tile
-//               scales / NCHW / int32 output; swizzled SMEM staging + TMA store.
+//               compile-time variants for the scale-only int8 (FAST 1-4) and
+//               fp32-digit (FAST 5) calls and for int8 with bias / act / per-m-tile
+//               scales (FAST 6), a runtime-generic one for NCHW / int32 output and
+//               the rest; swizzled SMEM staging + TMA store.
 //   warp 16     producer: B image bulk copies (once per n-tile), code tiles by TMA.
 //   warp 17     TMEM allocator; leader: MMA issuer (one elected lane, A from TMEM,
 //               B from SMEM); peer: forwards its generators' stage completions.
@@ -1162,8 +1163,9 @@ constexpr int kPProd = 16;   // producer (B image, code tiles)
 constexpr int kPMma = 17;    // TMEM allocator + MMA issuer (leader) / peer signaler
 constexpr int kPWatch = 18;  // leader: barrier watcher for the MMA issuer
 
-// FAST: compile-time plain epilogue (int8 tables, one scale, no bias / act /
-// int32 output, TMA-store staging): the generic epilogue's runtime-selected
+// FAST: compile-time epilogue variants (1-4: int8 tables, one scale, no bias /
+// act / int32 output; 5: fp32 digit planes; 6: int8 + bias / act / per-m-tile
+// scales; all TMA-store staging): the generic epilogue's runtime-selected
 // variants (bias, GELU, per-m-tile scales, digit recombination, direct
 // stores) inflate the kernel to ~200 KB of SASS and cost instruction-cache
 // misses and constant-bank reloads on every pass.
@@ -1603,7 +1605,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         const int npass = HC / pc;
         long long e2 = etr ? clock64() : 0;
         long long e3 = e2;
-        if (FAST == 4 && !(p.debug & 1)) {
+        if ((FAST == 4 || FAST == 6) && !(p.debug & 1)) {
           // one thread per accumulator half stores the half's 128-row boxes: it waits
           // until its previous stores have read the slab, then releases the half
           if (sub == 0) {
@@ -1725,17 +1727,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           __syncwarp();
           continue;
         }
-        if constexpr (FAST == 1 || FAST == 4) {
+        if constexpr (FAST == 1 || FAST == 4 || FAST == 6) {
           // 32 columns of this row: exact int -> f32, times the table scale,
-          // into the 128B-swizzled staging slab (one 32-column box)
+          // into the 128B-swizzled staging slab (one 32-column box).
+          // FAST 6 (the caller stacks): per-m-tile scale (scale_mtile % 32 == 0:
+          // one scale per pass), + bias, then the activation — the generic
+          // epilogue's operations in its order (fmul_rn, fadd_rn, act).
           const uint32_t dst = out_saddr + (uint32_t)(((h2 * 32) >> ib_log2) * (kRowsPerTile * ib * 4));
+          const int mp = m_base + hf * HC + h2 * 32;  // first real column of this pass
+          uint64_t sc2 = scale2;
+          if constexpr (FAST == 6) {
+            if (p.scale_mtile > 0) {
+              const float s = mp < p.M ? __ldg(p.scales + mp / p.scale_mtile) : 1.0f;
+              sc2 = pk_f2(s, s);
+            }
+          }
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             float f0, f1, f2, f3;
             const uint64_t b01 = pk_f2(__int_as_float(0x4B400000 + (int)v[4 * q]), __int_as_float(0x4B400000 + (int)v[4 * q + 1]));
             const uint64_t b23 = pk_f2(__int_as_float(0x4B400000 + (int)v[4 * q + 2]), __int_as_float(0x4B400000 + (int)v[4 * q + 3]));
-            up_f2(mul_f2(add_f2(b01, kNegMagic2), scale2), f0, f1);
-            up_f2(mul_f2(add_f2(b23, kNegMagic2), scale2), f2, f3);
+            up_f2(mul_f2(add_f2(b01, kNegMagic2), sc2), f0, f1);
+            up_f2(mul_f2(add_f2(b23, kNegMagic2), sc2), f2, f3);
+            if constexpr (FAST == 6) {
+              const int m = mp + 4 * q;  // M % 4 == 0: the 4 columns are wholly in or out
+              if (p.bias && m < p.M) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + m));
+                f0 = __fadd_rn(f0, b4.x);
+                f1 = __fadd_rn(f1, b4.y);
+                f2 = __fadd_rn(f2, b4.z);
+                f3 = __fadd_rn(f3, b4.w);
+              }
+              if (p.act) {
+                f0 = apply_act(f0, p.act);
+                f1 = apply_act(f1, p.act);
+                f2 = apply_act(f2, p.act);
+                f3 = apply_act(f3, p.act);
+              }
+            }
             sts_v4(dst + (uint32_t)((q ^ swz) << 4), f0, f1, f2, f3);
           }
           continue;
@@ -1844,7 +1873,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         }  // passes
         e3 = etr ? clock64() : 0;
         if (etl) TL(9, epi_unit);
-        if (FAST == 4 && !(p.debug & 49)) {
+        if ((FAST == 4 || FAST == 6) && !(p.debug & 49)) {
           fence_proxy_async_smem();
           if (sub != 0) {
             asm volatile("bar.arrive %0, 128;" ::"r"(6 + 2 * hf) : "memory");
@@ -2075,6 +2104,7 @@ static int launch_pair_k(const CUtensorMap& map, const CUtensorMap& omap, OneHot
                                    : epi == 2 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 2 : 0>
                                    : epi == 3 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 3 : 0>
                                    : epi == 4 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 4 : 0>
+                                   : epi == 6 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 6 : 0>
                                               : onehot_pair_kernel<K, DIGITS, 1, 4>)
                                 : onehot_pair_kernel<K, DIGITS, 1, 2>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -2216,6 +2246,12 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
       if (const char* e = getenv("LUTGPU_OH_EPI")) epi = atoi(e);
       if (epi < 0 || epi > 4) epi = 4;
     }
+    // int8 caller stacks (bias / GELU / ReLU / per-m-tile scales, the BERT and FFN
+    // layers): compile-time variant of the same per-half TMA-store epilogue
+    if (!plain && digits == 1 && p.sparse && p.stage_kb == 4 && out && !out_i32 && out_hw == 0 && g.NT == 64 &&
+        !(p.debug & 512) && (scale_mtile == 0 || scale_mtile % 32 == 0) &&
+        (reinterpret_cast<uintptr_t>(bias) & 15) == 0 && !(getenv("LUTGPU_OH_EPI") && atoi(getenv("LUTGPU_OH_EPI")) == 0))
+      epi = 6;
     // plain fp32 (4 digit planes): compile-time recombination epilogue, per-warp TMA stores
     if (digits == 4 && p.sparse && p.stage_kb == 4 && out && !out_i32 && !bias && !act && out_hw == 0 &&
         g.NT == 64 && !(p.debug & 512) && !(getenv("LUTGPU_OH_EPI") && atoi(getenv("LUTGPU_OH_EPI")) == 0))
@@ -2223,7 +2259,7 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
     const char* e5 = getenv("LUTGPU_OH_TMAOUT");
     if (!(e5 && e5[0] == '0') && out && out_hw == 0 && (M % 4) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
         ib >= 4 && half_cols % ib == 0 && base_smem + stage_bytes <= max_smem_optin()) {
-      if (make_tmap_2d_f32_box(&omap, out, (uint64_t)M, (uint64_t)n, (uint32_t)ib, epi == 4 ? kRowsPerTile : 32)) {
+      if (make_tmap_2d_f32_box(&omap, out, (uint64_t)M, (uint64_t)n, (uint32_t)ib, (epi == 4 || epi == 6) ? kRowsPerTile : 32)) {
         p.tma_out = 1;
         p.stage_slab = 1;
         p.epi = epi;
@@ -2231,6 +2267,10 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
     }
     if (p.epi == 2 && ((M % 128) != 0 || (reinterpret_cast<uintptr_t>(out) & 31) != 0)) p.epi = 1;
     if (p.epi == 4 && ib != 32) p.epi = 1;
+    if (p.epi == 6 && ib != 32) {  // unreachable at NT = 64: the generic epilogue stores 32-row boxes
+      p.epi = 0;
+      if (!make_tmap_2d_f32_box(&omap, out, (uint64_t)M, (uint64_t)n, (uint32_t)ib, 32)) p.tma_out = 0;
+    }
     if (p.epi == 1 && make_tmap_2d_f32_box(&omap, out, (uint64_t)M, (uint64_t)n, (uint32_t)ib, 32) == false) p.epi = 0;
     if (p.epi == 2 || p.epi == 3) p.tma_out = 0;
     const size_t smem = base_smem + (p.stage_slab ? stage_bytes : 0);

@@ -500,3 +500,32 @@ def test_conv_int8_tensor_nchw(L):
     want = O.lut_layer_infer(cols, books, q=q, scale=s).reshape(bsz, hh, ww, cout).transpose(0, 3, 1, 2)
     got = y.cpu().numpy() if isinstance(y, torch.Tensor) else np.asarray(y)
     assert got.tobytes() == np.ascontiguousarray(want).tobytes()
+
+
+@pytest.mark.parametrize("m,mtile", [(3072, 0), (3072, 128), (768, 32), (200, 64), (1000, 40)])
+@pytest.mark.parametrize("act", [None, "relu", "gelu"])
+def test_tc_stack_epilogue_bitwise(L, m, mtile, act):
+    """The pair kernel's compile-time caller-stack epilogue (int8 tables + bias,
+    ReLU / GELU, per-m-tile scales: configs[1]/[3] layers) against the CUDA-core
+    gather on the same device codes: bitwise (same fmul_rn, fadd_rn, activation
+    per element). mtile 40 is not a multiple of 32 and takes the generic epilogue."""
+    import torch
+
+    n, c, k, v = 2000, 24, 16, 32
+    g = torch.Generator(device="cuda").manual_seed(m + mtile)
+    a = torch.randn((n, c * v), generator=g, device="cuda")
+    books = torch.randn((c, k, v), generator=g, device="cuda")
+    w = torch.randn((c * v, m), generator=g, device="cuda") * 0.02
+    bias = torch.randn(m, generator=g, device="cuda") * 0.1
+    kw = dict(cfg=L.PqConfig(v=v, k=k), books=books, weight=w, bias=bias, qat=True, act=act, scale_mtile=mtile)
+    lt = L.LutLayer(gather="tensor", **kw)
+    lc = L.LutLayer(gather="cuda", **kw)
+    assert lt.uses_tensor_cores(True)
+    got = L.lut_layer_infer(a, lt, integer=True)
+    assert torch.equal(got, L.lut_layer_infer(a, lc, integer=True))
+    if act is None and mtile == 0:  # and against the oracle restatement
+        an, bn = a.cpu().numpy(), books.cpu().numpy()
+        table = O.build_table(w.cpu().numpy(), bn)
+        q, s = O.quantize_table(table)
+        want = O.lut_layer_infer(an, bn, q=q, scale=s, bias=bias.cpu().numpy())
+        assert got.cpu().numpy().tobytes() == want.tobytes()
