@@ -1742,6 +1742,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
               sc2 = pk_f2(s, s);
             }
           }
+          if constexpr (FAST == 6) {
+            // 16 values at a time, then the activation over all of them (16
+            // independent erf chains: with 8 epilogue warps per SM a per-4-column
+            // loop left the GELU latency-bound), then 4 staging stores
+#pragma unroll
+            for (int hb = 0; hb < 32; hb += 16) {
+              float f[16];
+#pragma unroll
+              for (int j = 0; j < 16; j += 2) {
+                const uint64_t b = pk_f2(__int_as_float(0x4B400000 + (int)v[hb + j]),
+                                         __int_as_float(0x4B400000 + (int)v[hb + j + 1]));
+                up_f2(mul_f2(add_f2(b, kNegMagic2), sc2), f[j], f[j + 1]);
+              }
+              if (p.bias) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const int m = mp + hb + 4 * q;  // M % 4 == 0: the 4 columns are wholly in or out
+                  if (m < p.M) {
+                    const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + m));
+                    f[4 * q] = __fadd_rn(f[4 * q], b4.x);
+                    f[4 * q + 1] = __fadd_rn(f[4 * q + 1], b4.y);
+                    f[4 * q + 2] = __fadd_rn(f[4 * q + 2], b4.z);
+                    f[4 * q + 3] = __fadd_rn(f[4 * q + 3], b4.w);
+                  }
+                }
+              }
+              if (p.act == LUT_ACT_GELU) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) f[j] = gelu_erf(f[j]);
+              } else if (p.act) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) f[j] = apply_act(f[j], p.act);
+              }
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                sts_v4(dst + (uint32_t)(((hb / 4 + q) ^ swz) << 4), f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+            }
+            continue;
+          }
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             float f0, f1, f2, f3;
@@ -1749,22 +1788,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             const uint64_t b23 = pk_f2(__int_as_float(0x4B400000 + (int)v[4 * q + 2]), __int_as_float(0x4B400000 + (int)v[4 * q + 3]));
             up_f2(mul_f2(add_f2(b01, kNegMagic2), sc2), f0, f1);
             up_f2(mul_f2(add_f2(b23, kNegMagic2), sc2), f2, f3);
-            if constexpr (FAST == 6) {
-              const int m = mp + 4 * q;  // M % 4 == 0: the 4 columns are wholly in or out
-              if (p.bias && m < p.M) {
-                const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + m));
-                f0 = __fadd_rn(f0, b4.x);
-                f1 = __fadd_rn(f1, b4.y);
-                f2 = __fadd_rn(f2, b4.z);
-                f3 = __fadd_rn(f3, b4.w);
-              }
-              if (p.act) {
-                f0 = apply_act(f0, p.act);
-                f1 = apply_act(f1, p.act);
-                f2 = apply_act(f2, p.act);
-                f3 = apply_act(f3, p.act);
-              }
-            }
             sts_v4(dst + (uint32_t)((q ^ swz) << 4), f0, f1, f2, f3);
           }
           continue;
