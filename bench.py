@@ -53,6 +53,10 @@ def parse():
     p.add_argument("--workload", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"], default="cfg5",
                    help="BASELINE configs[i-1]; cfg5 (default) is the headline scaling sweep")
     p.add_argument("--scale-mtile", type=int, default=0, help="cfg2/cfg4: per-m-tile int8 scales (0 = per table)")
+    p.add_argument("--no-variants", action="store_true", help="skip the K=64 / fp32 / CUDA-core variant timings")
+    p.add_argument("--no-ties", action="store_true", help="skip the f64 near-tie count")
+    p.add_argument("--gather-out", action="store_true",
+                   help="under torchrun: also time the NCCL all-gather of the row-sharded output")
     return p.parse_args()
 
 
@@ -72,19 +76,37 @@ def peaks():
 _CPU_WORK = None  # set before the fork pool starts; workers inherit it (no pickling in the timed loop)
 
 
-def _cpu_worker(_i):
+def _cpu_worker(rows):
     from oracle import lut_oracle as O
 
     a, books, table, q, scale, integer = _CPU_WORK
+    a = a[:rows]
     if integer:
         return O.lut_layer_infer(a, books, q=q, scale=scale).shape[0]
     return O.lut_layer_infer(a, books, table=table, integer=False).shape[0]
 
 
-def cpu_reference(dim, m, v, k, integer, rows_per_core, steps, warmup, seed=7):
+def _cpu_pool_time(rows_per_core, workers, steps, warmup, ctx):
+    """Median seconds per step of `workers` processes each running rows_per_core rows."""
+    times = []
+    with ctx.Pool(workers) as pool:
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            done = sum(pool.map(_cpu_worker, [rows_per_core] * workers, chunksize=1))
+            assert done == rows_per_core * workers
+            dt = time.perf_counter() - t0
+            if i >= warmup:
+                times.append(dt)
+    return statistics.median(times), len(times)
+
+
+def cpu_reference(dim, m, v, k, integer, rows_per_core, steps, warmup, seed=7, extras=True):
     """The reference's CPU path (oracle port of lutkit.kernels.lut_layer_infer,
-    encode in f64 + ascending-c gather) on all host cores, rows sharded over
-    a process pool (one BLAS thread per process, as the reference caps it)."""
+    f64 encode + ascending-c gather) on the host cores: rows sharded over a
+    process pool, one BLAS thread per process, as the reference caps BLAS
+    (__init__.py:12-15).  `extras`: the reference's own single-core contract
+    (one process) and a linearity check (the pool at half the sample; rows/s
+    must agree within 15% for the sample to stand in for the 2^20-row shard)."""
     import multiprocessing as mp
 
     from oracle import lut_oracle as O
@@ -102,21 +124,23 @@ def cpu_reference(dim, m, v, k, integer, rows_per_core, steps, warmup, seed=7):
     global _CPU_WORK
     _CPU_WORK = (shard, books, table, q, scale, integer)
     ctx = mp.get_context("fork")
-    times = []
-    with ctx.Pool(cores) as pool:
-        for i in range(warmup + steps):
-            t0 = time.perf_counter()
-            done = sum(pool.map(_cpu_worker, range(cores), chunksize=1))
-            assert done == rows_per_core * cores
-            dt = time.perf_counter() - t0
-            if i >= warmup:
-                times.append(dt)
+    med, nsteps = _cpu_pool_time(rows_per_core, cores, steps, warmup, ctx)
     rows = rows_per_core * cores
-    med = statistics.median(times)
-    return {"value": rows / med, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{rows} rows ({rows_per_core}/core) of the same layer, median of {len(times)} steps; "
-                      f"oracle port of lutkit lut_layer_infer ({'int8' if integer else 'f32'} tables)",
-            "seconds_per_step": med, "rows": rows}
+    res = {"value": rows / med, "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": f"{rows} rows ({rows_per_core}/core) of the same layer per step, median of {nsteps} steps "
+                     f"after {warmup} warm-up; oracle port of lutkit lut_layer_infer "
+                     f"({'int8' if integer else 'f32'} tables)",
+           "seconds_per_step": med, "rows_sampled": rows, "steps": nsteps, "warmup": warmup}
+    if extras:
+        half = max(1, rows_per_core // 2)
+        med_h, _ = _cpu_pool_time(half, cores, 1, 0, ctx)
+        r_half = half * cores / med_h
+        res["linearity"] = {"rows_sampled_half": half * cores, "rows_per_s_half": r_half,
+                            "ratio_full_over_half": res["value"] / r_half,
+                            "linear": abs(res["value"] / r_half - 1.0) < 0.15}
+        med_1, _ = _cpu_pool_time(half, 1, 1, 0, ctx)
+        res["one_core"] = {"value": half / med_1, "unit": UNIT, "cores": 1, "rows_sampled": half}
+    return res
 
 
 # ------------------------------------------------------------- clocks
@@ -176,6 +200,145 @@ class ClockSampler:
 # ------------------------------------------------------------- GPU side
 
 
+def near_tie_count(a, books, chunk):
+    """(row, codebook) pairs whose best and second-best literal f64 distances
+    (pq.py:53-73) lie within 1e-6 relative: the north star's documented
+    near-tie class.  torch f64 on the device, outside the timed region."""
+    import torch
+
+    n = a.shape[0]
+    c, k, v = books.shape
+    p64 = books.double()[None]
+    near = 0
+    for r0 in range(0, n, chunk):
+        r1 = min(n, r0 + chunk)
+        d = torch.sub(a[r0:r1].double().view(r1 - r0, c, 1, v), p64).square_().sum(-1)
+        two = d.topk(2, dim=-1, largest=False).values
+        gap = (two[..., 1] - two[..., 0]) / torch.clamp(torch.maximum(two[..., 0].abs(), two[..., 1].abs()),
+                                                      min=1e-300)
+        near += int((gap < 1e-6).sum())
+        del d, two, gap
+    return near
+
+
+class Cfg5:
+    """One configs[4] layer variant (K, table kind, engine) over the rank's
+    resident rows, timed with CUDA events on the launching stream."""
+
+    def __init__(self, L, lib, dev, a, codes, out, near, d, m, v, k, integer, gather, digits, seed=1234):
+        import torch
+
+        self.lib, self.a, self.codes, self.out, self.near = lib, a, codes, out, near
+        self.n, self.d, self.m, self.v, self.k, self.c = a.shape[0], d, m, v, k, d // v
+        self.integer = integer
+        g = torch.Generator(device=dev).manual_seed(seed)
+        self.books = torch.randn((self.c, k, v), generator=g, device=dev)
+        w = torch.randn((d, m), generator=g, device=dev) / math.sqrt(d)
+        self.layer = L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=self.books, weight=w, qat=integer, gather=gather,
+                                f32_digits=digits)
+        self.tensor = self.layer.uses_tensor_cores(integer)
+        self.digits = digits
+        self.scales = self.layer.qtable.scales_tensor(dev) if integer else None
+        self.image = self.layer.onehot_image(integer) if self.tensor else None
+        self.cstride = int(lib.lut_code_stride(self.c))
+        self.engine = ("tcgen05 one-hot kind::i8" + ("" if integer else f", {digits} digit planes")) \
+            if self.tensor else "CUDA-core SMEM gather"
+
+    def step(self, stream, ev=None):
+        """encode -> lookup-aggregate: the two kernels of lut_layer_forward, timed apart."""
+        from paper_2302_03213_b200._lib import check
+
+        lib, sp, n, c, k, m = self.lib, stream.cuda_stream, self.n, self.c, self.k, self.m
+        if ev:
+            ev[0].record(stream)
+        check(lib.lut_encode_f32(self.a.data_ptr(), n, self.d, self.layer.books_prep.data_ptr(), c, k, self.v,
+                                 self.codes.data_ptr(), 8, self.cstride, self.near.data_ptr(), sp))
+        if ev:
+            ev[1].record(stream)
+        if self.tensor:
+            check(lib.lut_gather_onehot(self.codes.data_ptr(), self.cstride, n, c, k, m,
+                                        1 if self.integer else self.digits, self.image.data_ptr(),
+                                        self.scales.data_ptr() if self.integer else None, 0, None, 0,
+                                        self.out.data_ptr(), None, 0, sp))
+        elif self.integer:
+            check(lib.lut_gather_i8(self.codes.data_ptr(), 8, n, c, k, m, self.layer.qtable.q.data_ptr(),
+                                    self.scales.data_ptr(), 0, None, 0, self.out.data_ptr(), None, 0, None, sp))
+        else:
+            check(lib.lut_gather_f32(self.codes.data_ptr(), 8, n, c, k, m, self.layer.table.data_ptr(), None, 0,
+                                     self.out.data_ptr(), 0, None, sp))
+        if ev:
+            ev[2].record(stream)
+
+    def bytes(self):
+        """Algorithmic HBM bytes per launch: gather reads codes
+        + table once and writes the output; encode reads A + codebooks and
+        writes codes; the layer reads A once and writes the output once."""
+        n, c, k, m, d, v = self.n, self.c, self.k, self.m, self.d, self.v
+        s = 1 if self.integer else 4
+        return {"gather": n * c + s * c * k * m + 4 * n * m, "encode": 4 * n * d + n * c + 4 * c * k * v,
+                "layer": 4 * n * d + s * c * k * m + 4 * c * k * v + 4 * n * m}
+
+    def time(self, steps, warmup, world=1, clocks=None):
+        import torch
+        import torch.distributed as dist
+
+        stream = torch.cuda.current_stream()
+        for _ in range(warmup):
+            self.step(stream)
+        torch.cuda.synchronize()
+        self.near.zero_()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with (clocks or _Null()):
+            t0.record(stream)
+            for i in range(steps):
+                torch.cuda.nvtx.range_push(f"step {i}")
+                self.step(stream, evs[i])
+                torch.cuda.nvtx.range_pop()
+            t1.record(stream)
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = t0.elapsed_time(t1)
+        enc = sum(e[0].elapsed_time(e[1]) for e in evs) / steps
+        gat = sum(e[1].elapsed_time(e[2]) for e in evs) / steps
+        return ms / steps, enc, gat
+
+    def roofline(self, enc_ms, gat_ms, step_ms, hbm_peak, peak_kind):
+        b = self.bytes()
+        dom, dom_ms = ("gather", gat_ms) if gat_ms >= enc_ms else ("encode", enc_ms)
+        achieved = b[dom] / (dom_ms / 1e3) / 1e9
+        r = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+             "traffic": None, "kernel": dom, "peak_kind": peak_kind, "algorithmic_bytes": b[dom],
+             "kernel_ms": {"encode": enc_ms, "gather": gat_ms},
+             "kernel_frac": {"encode": b["encode"] / (enc_ms / 1e3) / 1e9 / hbm_peak,
+                             "gather": b["gather"] / (gat_ms / 1e3) / 1e9 / hbm_peak},
+             "layer_hbm_floor_ms": b["layer"] / (hbm_peak * 1e9) * 1e3,
+             "layer_frac_of_hbm_floor": (b["layer"] / (hbm_peak * 1e9) * 1e3) / step_ms}
+        if self.tensor:
+            # the one-hot GEMM's own ceiling: 2:4-sparse kind::i8, 16384 logical MAC/clk/SM
+            macs = self.n * self.m * self.c * self.k * (1 if self.integer else self.digits)
+            floor = macs / (16384 * 148 * 1.965e9) * 1e3
+            r["sparse_mma_floor_ms"] = floor
+        else:
+            # CUDA-core gather: table lookups from SMEM, 128 B/clk/SM
+            lookups = self.n * self.m * self.c * (1 if self.integer else 4)
+            r["smem_lookup"] = {"bytes": lookups, "floor_ms": lookups / (148 * 128 * 1.965e9) * 1e3,
+                                "frac": (lookups / (148 * 128 * 1.965e9) * 1e3) / gat_ms}
+        return r
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
 def main():
     args = parse()
     if args.workload != "cfg5":
@@ -196,13 +359,15 @@ def main():
         if rank != 0:
             return
         ref = cpu_reference(d, m, v, k, integer, rows_per_core=args.cpu_rows or (4096 if integer else 2048),
-                            steps=max(1, args.steps), warmup=max(0, min(args.warmup, 1)))
+                            steps=max(1, args.steps), warmup=max(0, args.warmup))
+        config["rows_sampled_per_step"] = ref["rows_sampled"]
         eff = 2.0 * d * m * ref["value"] / 1e9
         line = {"impl": "reference", "metric": METRIC, "value": ref["value"], "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ref["seconds_per_step"] * 1e3,
+                "steps": ref["steps"], "warmup": ref["warmup"], "ms_per_step": ref["seconds_per_step"] * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
                 "data": "synthetic", "config": config, "effective_gops": eff,
                 "cpu_baseline": {k_: ref[k_] for k_ in ("value", "unit", "cores", "kind", "sample")},
+                "one_core": ref.get("one_core"), "linearity": ref.get("linearity"),
                 "e2e": {"value": ref["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -216,120 +381,95 @@ def main():
     import torch.distributed as dist
 
     import paper_2302_03213_b200 as L
-    from paper_2302_03213_b200 import _device as D
-    from paper_2302_03213_b200._lib import check, load
+    from paper_2302_03213_b200._lib import load
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or os.environ.get("RANK") is not None:  # under torchrun, even at N = 1
         dist.init_process_group("nccl", device_id=dev)
     lib = load()
 
-    # ---- layer (replicated) and this rank's rows (generated on device from (seed, rank))
-    g = torch.Generator(device=dev).manual_seed(1234)
-    books = torch.randn((c, k, v), generator=g, device=dev)
-    w = torch.randn((d, m), generator=g, device=dev) / math.sqrt(d)
-    layer = L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=books, weight=w, qat=integer, gather=args.gather,
-                       f32_digits=args.digits)
-    tensor = layer.uses_tensor_cores(integer)
-    config["gather"] = ("tcgen05 one-hot kind::i8" + ("" if integer else f", {args.digits} digit planes")) \
-        if tensor else "CUDA-core SMEM gather"
+    # ---- this rank's rows (generated on device from (seed, rank)), shared buffers
     n = args.rows
     ga = torch.Generator(device=dev).manual_seed(99 + rank)
     a = torch.randn((n, d), generator=ga, device=dev)
-    cstride = int(lib.lut_code_stride(c))
-    codes = torch.empty((n, cstride), dtype=torch.uint8, device=dev)
+    codes = torch.empty((n, int(lib.lut_code_stride(c))), dtype=torch.uint8, device=dev)
     out = torch.empty((n, m), dtype=torch.float32, device=dev)
     near = torch.zeros(1, dtype=torch.int32, device=dev)
-    scales = layer.qtable.scales_tensor(dev) if integer else None
-    image = layer.onehot_image(integer) if tensor else None
-    stream = torch.cuda.current_stream()
-    sp = stream.cuda_stream
-    desc = layer.desc(integer)
-
-    def step(ev=None):
-        # encode -> lookup-aggregate, the two kernels of lut_layer_forward, timed apart
-        if ev:
-            ev[0].record(stream)
-        check(lib.lut_encode_f32(a.data_ptr(), n, d, layer.books_prep.data_ptr(), c, k, v, codes.data_ptr(), 8,
-                                 cstride, near.data_ptr(), sp))
-        if ev:
-            ev[1].record(stream)
-        if tensor:
-            check(lib.lut_gather_onehot(codes.data_ptr(), cstride, n, c, k, m, 1 if integer else args.digits,
-                                        image.data_ptr(), scales.data_ptr() if integer else None, 0, None, 0,
-                                        out.data_ptr(), None, 0, sp))
-        elif integer:
-            check(lib.lut_gather_i8(codes.data_ptr(), 8, n, c, k, m, layer.qtable.q.data_ptr(), scales.data_ptr(),
-                                    0, None, 0, out.data_ptr(), None, 0, None, sp))
-        else:
-            check(lib.lut_gather_f32(codes.data_ptr(), 8, n, c, k, m, layer.table.data_ptr(), None, 0,
-                                     out.data_ptr(), 0, None, sp))
-        if ev:
-            ev[2].record(stream)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    near.zero_()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    hbm_peak, _, peak_kind = peaks()
+    run = Cfg5(L, lib, dev, a, codes, out, near, d, m, v, k, integer, args.gather, args.digits)
+    config["gather"] = run.engine
     with ClockSampler(local) as clocks:
-        t_start.record(stream)
-        for i in range(args.steps):
-            step(evs[i])
-        t_end.record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = t_start.elapsed_time(t_end)
-    enc_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
-    gat_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        ms_step, enc_ms, gat_ms = run.time(args.steps, args.warmup, world)
+    in_dist = dist.is_available() and dist.is_initialized()
+    if in_dist and world > 1:
+        t = torch.tensor([ms_step], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_step = ms / args.steps
+        ms_step = float(t.item())
+    redecided = int(near.item())
     rows_total = n * world
     value = rows_total / (ms_step / 1e3)
     eff_gops = 2.0 * d * m * value / 1e9
-    near_ties = int(near.item())
+    roofline = run.roofline(enc_ms, gat_ms, ms_step, hbm_peak, peak_kind)
+    for rnd in ("r02", "r01"):  # DRAM bytes per launch from the newest committed ncu capture
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "ncu_traffic.json")) as f:
+                tr = json.load(f)
+            tc = tr["config"]
+            if (tc["d"], tc["m"], tc["v"], tc["k"], tc["table"]) == (d, m, v, k, args.table) and run.tensor:
+                roofline["traffic"] = tr[f"{roofline['kernel']}_dram_bytes"] / tr["rows"] * n
+                roofline["traffic_source"] = f"profiles/{rnd}/ncu_traffic.json"
+                break
+        except (OSError, KeyError, ValueError):
+            continue
 
-    # ---- roofline of the dominant kernel (algorithmic bytes per launch / event time)
-    hbm_peak, sm_mhz_max, peak_kind = peaks()
-    s = 1 if integer else 4
-    gather_bytes = n * c + s * c * k * m + 4 * n * m
-    encode_bytes = 4 * n * d + n * c + 4 * c * k * v
-    lookups = n * m * c
-    smem_peak = 148 * 128 * sm_mhz_max * 1e6  # B/s, LDS bandwidth at max clock
-    if gat_ms >= enc_ms:
-        dom, dom_ms, dom_bytes = "gather", gat_ms, gather_bytes
-    else:
-        dom, dom_ms, dom_bytes = "encode", enc_ms, encode_bytes
-    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
-    layer_hbm = 4 * n * d + s * c * k * m + 4 * c * k * v + 4 * n * m
-    traffic = None  # DRAM bytes per launch of the dominant kernel, from the committed ncu capture
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as f:
-            tr = json.load(f)
-        tc = tr["config"]
-        if (tc["d"], tc["m"], tc["v"], tc["k"], tc["table"]) == (d, m, v, k, args.table) and tensor:
-            traffic = tr[f"{dom}_dram_bytes"] / tr["rows"] * n
-    except (OSError, KeyError, ValueError):
-        pass
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": traffic, "kernel": dom, "peak_kind": peak_kind,
-                "algorithmic_bytes": dom_bytes,
-                "kernel_ms": {"encode": enc_ms, "gather": gat_ms},
-                "smem_lookup": {"bytes": lookups * s, "achieved_TBps": lookups * s / (gat_ms / 1e3) / 1e12,
-                                "peak_TBps": smem_peak / 1e12,
-                                "frac": (lookups * s / (gat_ms / 1e3)) / smem_peak},
-                "layer_hbm_floor_ms": layer_hbm / (hbm_peak * 1e9) * 1e3,
-                "layer_frac_of_hbm_floor": (layer_hbm / (hbm_peak * 1e9) * 1e3) / ms_step}
+    # ---- north-star near ties (f64 gap < 1e-6 relative), counted over every row (untimed)
+    near_1e6 = near_tie_count(a, run.books, chunk=2048 if k <= 16 else 512) if not args.no_ties else None
+
+    # ---- other configs[4] variants on the same rows (BASELINE: K in {16, 64}, fp32 and int8 tables)
+    variants = {}
+    if not args.no_variants and world == 1:
+        del run
+        torch.cuda.empty_cache()
+        for name, kk, intg, gth in (("k64_i8_tensor", 64, True, "tensor"), ("f32_tensor_4digit", 16, False, "tensor"),
+                                    ("f32_cuda_bitwise", 16, False, "cuda"), ("i8_cuda", 16, True, "cuda")):
+            if (kk, intg, gth) == (k, integer, args.gather):
+                continue
+            vr = Cfg5(L, lib, dev, a, codes, out, near, d, m, v, kk, intg, gth, 4)
+            st_ms, e_ms, g_ms = vr.time(max(2, args.steps // 4), 2)
+            rf = vr.roofline(e_ms, g_ms, st_ms, hbm_peak, peak_kind)
+            variants[name] = {"engine": vr.engine, "ms_per_step": st_ms, "rows_per_s": n / (st_ms / 1e3),
+                              "kernel_ms": rf["kernel_ms"], "kernel_frac": rf["kernel_frac"],
+                              "layer_frac_of_hbm_floor": rf["layer_frac_of_hbm_floor"],
+                              **({"sparse_mma_floor_ms": rf["sparse_mma_floor_ms"]} if "sparse_mma_floor_ms" in rf
+                                 else {"smem_lookup": rf["smem_lookup"]})}
+            del vr
+            torch.cuda.empty_cache()
+        run = Cfg5(L, lib, dev, a, codes, out, near, d, m, v, k, integer, args.gather, args.digits)
+        run.step(torch.cuda.current_stream())  # the headline layer's output back in `out` for the e2e check
+
+    # ---- optional all-gather of the row-sharded output, timed apart
+    gathered = None
+    if args.gather_out and in_dist:
+        from paper_2302_03213_b200.dist import gather_rows
+
+        rows_g = min(n, 1 << 17)
+        part = out[:rows_g]
+        gather_rows(part, rows_g * world)  # warm NCCL
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        e0.record()
+        full = gather_rows(part, rows_g * world)
+        e1.record()
+        torch.cuda.synchronize()
+        g_ms = e0.elapsed_time(e1)
+        t = torch.tensor([g_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        g_ms = float(t.item())
+        gathered = {"rows_per_rank": rows_g, "bytes_out_per_rank": full.numel() * 4, "ms": g_ms,
+                    "algbw_GBps": full.numel() * 4 / (g_ms / 1e3) / 1e9, "collective": "NCCL all_gather"}
+        del full
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
@@ -342,19 +482,19 @@ def main():
         a_h.copy_(a[:ne])
         o_h = torch.empty((ne, m), dtype=torch.float32, pin_memory=True)
         a_np, o_np = a_h.numpy(), o_h.numpy()
-        L.lut_layer_infer(a_np[: 1 << 14], layer, integer=integer)  # warm the executor
-        if world > 1:
+        L.lut_layer_infer(a_np[: 1 << 14], run.layer, integer=integer)  # warm the executor
+        if in_dist:
             dist.barrier()
         times = []
         for i in range(args.e2e_steps + 1):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            L.lut_layer_infer(a_np, layer, integer=integer, out=o_np)
+            L.lut_layer_infer(a_np, run.layer, integer=integer, out=o_np)
             t1 = time.perf_counter()
             if i:
                 times.append(t1 - t0)
         e2e_s = statistics.median(times)
-        if world > 1:
+        if in_dist and world > 1:
             t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
@@ -364,7 +504,7 @@ def main():
                "api": "paper_2302_03213_b200.lut_layer_infer(numpy pinned) -> lut_pipeline_run"}
         del a_h, o_h
 
-    if world > 1:
+    if in_dist:
         dist.destroy_process_group()
     if rank != 0:
         return
@@ -372,12 +512,17 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if not integer else "f32-encode/int8-table/int32-acc",
             "data": "synthetic (seeded torch.randn on device; random-init centroids/weights)",
-            "config": config, "effective_gops": eff_gops, "near_ties": near_ties,
-            "near_tie_rate": near_ties / (n * c * args.steps),
+            "config": config, "effective_gops": eff_gops,
+            "near_ties_gap_lt_1e6": near_1e6,
+            "near_ties_gap_lt_1e6_rate": None if near_1e6 is None else near_1e6 / (n * c),
+            "f64_redecisions": redecided // max(1, args.steps), "f64_redecision_rate": redecided / (n * c * args.steps),
             "roofline": roofline, "clocks": clocks.summary(), "gpu_launches": 2 * args.steps,
-            "e2e": e2e, "cpu_baseline": None}
+            "variants": variants or None, "gathered_out": gathered,
+            "e2e": e2e, "cpu_baseline": None, "launcher": "torchrun" if os.environ.get("RANK") is not None else "python"}
     if cpu is not None:
         line["cpu_baseline"] = {k_: cpu[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
+        line["cpu_baseline"]["one_core"] = cpu.get("one_core")
+        line["cpu_baseline"]["linearity"] = cpu.get("linearity")
     print(json.dumps(line), flush=True)
 
 

@@ -5,10 +5,26 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <mutex>
 #include <string>
 
 #include "common.cuh"
+
+namespace {
+// NVTX range around the host side of a launch (header-only nvtx3: a no-op
+// unless a profiler is attached)
+struct NvtxRange {
+  bool open = true;
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  void pop() {
+    if (open) nvtxRangePop();
+    open = false;
+  }
+  ~NvtxRange() { pop(); }
+};
+}  // namespace
 
 namespace lutgpu {
 
@@ -154,7 +170,7 @@ static int check_act(int act) {
 static int force_generic_env() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("LUTGPU_FORCE_GENERIC");
+    const char* e = probe_env("LUTGPU_FORCE_GENERIC");
     v = (e && e[0] == '1') ? 1 : 0;
   }
   return v;
@@ -372,8 +388,11 @@ int lut_layer_forward(const lut_layer_desc* L, const float* a, int64_t n, float*
   cudaStream_t s = (cudaStream_t)stream;
   const int d = L->c * L->v;
   const int64_t stride = lut_code_stride(L->c);
+  NvtxRange r_enc("lut.encode");
   LUT_TRY(encode_dense(a, n, d, static_cast<const float*>(L->books_prep), L->c, L->k, L->v, codes_scratch, 8, stride,
                        near_tie_count, s, force_generic_env()));
+  r_enc.pop();
+  NvtxRange r_gat("lut.gather");
   if (L->onehot_image) {
     const int digits = L->integer ? 1 : L->onehot_digits;
     return onehot_gather(codes_scratch, stride, n, L->c, L->k, L->m, digits, L->onehot_image, L->scales,
@@ -485,6 +504,7 @@ int lut_pipeline_run(lut_pipeline* p, const lut_layer_desc* L, const float* a_ho
     if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_comp, p->ev_in[b], 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_comp, p->ev_out[b], 0);
     if (e != cudaSuccess) break;
+    NvtxRange r_chunk("lut.pipeline.chunk");
     status = lut_layer_forward(L, p->dA[b], rows, p->dOut[b], p->dCodes[b], p->dNear, (lut_stream_t)p->s_comp);
     if (status != LUT_OK) break;
     e = cudaEventRecord(p->ev_comp[b], p->s_comp);

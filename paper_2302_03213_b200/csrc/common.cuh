@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <string>
 
@@ -19,6 +20,18 @@ int fail(int status, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);
 int num_sms();
 size_t max_smem_optin();
+
+// Tuning / ablation knobs (LUTGPU_OH_*, LUTGPU_ENC_*, ...) are read only in
+// probe builds (-DLUTGPU_PROBES, tools/build_probes.sh); the product build never
+// consults the environment on a call path.
+inline const char* probe_env(const char* name) {
+#ifdef LUTGPU_PROBES
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 #define LUT_CHECK_LAUNCH(where)                              \
   do {                                                       \

@@ -818,9 +818,9 @@ static int launch_tma(const float* a, int64_t n, int d, const float* prep, int C
   p.stages = stages;
   p.stage_bytes = stage_bytes;
   {
-    const char* e = getenv("LUTGPU_ENC_DEBUG");
+    const char* e = probe_env("LUTGPU_ENC_DEBUG");
     p.debug = e ? atoi(e) : 0;
-    const char* st = getenv("LUTGPU_ENC_STAGES");
+    const char* st = probe_env("LUTGPU_ENC_STAGES");
     if (st && atoi(st) >= 2 && atoi(st) <= stages) p.stages = stages = atoi(st);
   }
   p.ntiles = (n + kTileRows - 1) / kTileRows;
@@ -837,8 +837,8 @@ static int launch_tma(const float* a, int64_t n, int d, const float* prep, int C
   const size_t smem = (size_t)stages * stage_bytes + 2 * stages * sizeof(uint64_t) + 1024;
   // rows per lane (LUTGPU_ENC_RPL = 2 or 4; default 2), accumulator form (LUTGPU_ENC_CHAIN = 0 or 1)
   int rpl = 2, chain = 1;
-  if (const char* r = getenv("LUTGPU_ENC_RPL")) rpl = atoi(r) == 4 ? 4 : 2;
-  if (const char* c = getenv("LUTGPU_ENC_CHAIN")) chain = atoi(c) == 0 ? 0 : 1;
+  if (const char* r = probe_env("LUTGPU_ENC_RPL")) rpl = atoi(r) == 4 ? 4 : 2;
+  if (const char* c = probe_env("LUTGPU_ENC_CHAIN")) chain = atoi(c) == 0 ? 0 : 1;
   auto kern = rpl == 2 ? (chain ? encode_tma_kernel<V, 8, 2, 1> : encode_tma_kernel<V, 8, 2, 0>)
                        : (chain ? encode_tma_kernel<V, 4, 4, 1> : encode_tma_kernel<V, 4, 4, 0>);
   const int threads = rpl == 2 ? 9 * 32 : 5 * 32;
@@ -857,7 +857,7 @@ int encode_dense(const float* a, int64_t n, int d, const float* prep, int C, int
                  int code_bits, int64_t code_stride, int* near_tie, cudaStream_t stream, int force_generic) {
   if (n == 0 || C == 0) return LUT_OK;
   const bool aligned = (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (reinterpret_cast<uintptr_t>(prep) & 15) == 0;
-  if (!force_generic && aligned && !(getenv("LUTGPU_ENC_TC") && getenv("LUTGPU_ENC_TC")[0] == '0')) {
+  if (!force_generic && aligned && !(probe_env("LUTGPU_ENC_TC") && probe_env("LUTGPU_ENC_TC")[0] == '0')) {
     bool used = false;
     const int st = encode_dense_tc(a, n, d, prep, C, K, V, codes, code_bits, code_stride, near_tie, stream, &used);
     if (st != LUT_OK) return st;
@@ -888,7 +888,7 @@ int encode_conv(const float* x, int batch, int cin, int h, int w, int kh, int kw
   if (n == 0 || C == 0) return LUT_OK;
   ConvRows rows{x, cin, h, w, kh, kw, stride, pad, ho, wo};
   const int64_t code_stride = code_bits == 4 ? (C + 1) / 2 : C;
-  const char* force = getenv("LUTGPU_CONV_GENERIC");
+  const char* force = probe_env("LUTGPU_CONV_GENERIC");
   if (code_bits == 8 && kh == 3 && kw == 3 && V == 9 && C == cin && !(force && atoi(force))) {
     bool used = false;
     int st = LUT_OK;

@@ -408,7 +408,7 @@ int encode_dense_tc(const float* a, int64_t n, int d, const float* prep, int C, 
   const int nsm = num_sms();
   const int grid = (int)(p.nunits < nsm ? p.nunits : nsm);
   int gr = K == 16 ? 3 : 4;  // consumer groups (LUTGPU_ENC_TC_GROUPS = 2, 3 or 4)
-  if (const char* g = getenv("LUTGPU_ENC_TC_GROUPS")) gr = atoi(g) == 2 ? 2 : atoi(g) == 3 ? 3 : 4;
+  if (const char* g = probe_env("LUTGPU_ENC_TC_GROUPS")) gr = atoi(g) == 2 ? 2 : atoi(g) == 3 ? 3 : 4;
   int stages;
   void (*kern)(const CUtensorMap, const EncTcParams);
   if (K == 16) {

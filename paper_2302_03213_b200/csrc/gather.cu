@@ -398,7 +398,7 @@ static int launch_tiled(void (*kern)(GatherArgs, const T*), int nmt, size_t smem
   // CTAs per m-tile: each re-stages its m-tile's table slice, so with few rows cap
   // the split at ~min_rows rows per CTA (LUTGPU_GATHER_MINROWS; 0 = no cap)
   int64_t min_rows = 256;
-  if (const char* e = getenv("LUTGPU_GATHER_MINROWS")) min_rows = atoll(e);
+  if (const char* e = probe_env("LUTGPU_GATHER_MINROWS")) min_rows = atoll(e);
   int cpm = nmt >= slots ? 1 : slots / nmt;
   if (min_rows > 0) {
     const int64_t cap = (g.n + min_rows - 1) / min_rows;
@@ -421,7 +421,7 @@ int gather_f32_strided(const uint8_t* codes, int code_bits, int64_t code_stride,
   // m-tile width: the widest slice that fits; with few rows prefer narrower
   // slices (more m-tiles, each CTA stages less) until the m-tiles fill the chip
   int mt_cap = 64;
-  if (const char* e = getenv("LUTGPU_GATHER_MT")) mt_cap = atoi(e);
+  if (const char* e = probe_env("LUTGPU_GATHER_MT")) mt_cap = atoi(e);
   else if (n < 65536) {
     const int floor_mt = n < 16384 ? 8 : 16;
     while (mt_cap > floor_mt && (M + mt_cap - 1) / mt_cap < num_sms()) mt_cap /= 2;

@@ -44,6 +44,17 @@
 
 namespace lutgpu {
 
+// Ablation bits and role counters exist only in probe builds (-DLUTGPU_PROBES,
+// tools/build_probes.sh): in the product build they are compile-time zero, so
+// no check of them reaches the issued code.
+#ifdef LUTGPU_PROBES
+#define OH_DEBUG(p) ((p).debug)
+#define OH_TRACE(p) ((p).trace)
+#else
+#define OH_DEBUG(p) 0
+#define OH_TRACE(p) static_cast<unsigned long long*>(nullptr)
+#endif
+
 constexpr int kOhThreads = 14 * 32;  // producer, MMA, 8 generators, 4 epilogue
 constexpr int kRowsPerTile = 128;
 constexpr int kKB = 128;       // K bytes per A stage / B block
@@ -190,12 +201,6 @@ __device__ __forceinline__ void tmem_ld16_at(uint32_t taddr, uint32_t (&v)[64]) 
         "=r"(v[OFF + 12]), "=r"(v[OFF + 13]), "=r"(v[OFF + 14]), "=r"(v[OFF + 15])
       : "r"(taddr)
       : "memory");
-}
-
-// exact int32 -> f32 for |x| < 2^22 on the FMA/ALU pipes (I2F is quarter rate):
-// the float with bits 0x4B400000 + x is 12582912 + x exactly.
-__device__ __forceinline__ float i2f_exact(uint32_t x) {
-  return __fsub_rn(__int_as_float(0x4B400000 + (int)x), 12582912.0f);
 }
 
 __device__ __forceinline__ uint64_t pk_f2(float lo, float hi) {
@@ -605,10 +610,10 @@ __device__ __forceinline__ unsigned long long gtime() {
     if (p.tl && blockIdx.x < 2 && (int)(idx) >= 0 && (int)(idx) < kTlN)                             \
       p.tl[((int)blockIdx.x * kTlEv + (ev)) * kTlN + (int)(idx)] = gtime();                          \
   } while (0)
-#define OH_T0(var) long long var = (p.trace && blockIdx.x == 0) ? clock64() : 0
+#define OH_T0(var) long long var = (OH_TRACE(p) && blockIdx.x == 0) ? clock64() : 0
 #define OH_ACC(slot, var) \
   do {                    \
-    if (p.trace && blockIdx.x == 0 && lane == 0) atomicAdd(p.trace + (slot), (unsigned long long)(clock64() - var)); \
+    if (OH_TRACE(p) && blockIdx.x == 0 && lane == 0) atomicAdd(OH_TRACE(p) + (slot), (unsigned long long)(clock64() - var)); \
   } while (0)
 #else
 #define TL(ev, idx) \
@@ -765,11 +770,11 @@ __global__ void __launch_bounds__(kOhThreads, 1)
       for (int st = 0; st < nst; ++st) {
         {
           OH_T0(t0);
-          if (!(p.debug & 8)) mbar_wait(&a_full[as], aph);
+          if (!(OH_DEBUG(p) & 8)) mbar_wait(&a_full[as], aph);
           OH_ACC(2, t0);
         }
         tc_fence_after();
-        if (!(p.debug & 2)) {
+        if (!(OH_DEBUG(p) & 2)) {
           const uint64_t bd = b_desc0 + (uint64_t)((2 * st * p.NT * kKB) >> 4);
           const uint32_t a_tmem = tmem_base + a_col0 + as * SC;
           if constexpr (SP)
@@ -815,7 +820,7 @@ __global__ void __launch_bounds__(kOhThreads, 1)
       }
       const uint32_t row_saddr = smem_u32(code_smem + cs * code_tile_bytes) + row_in_tile * 128;
       const uint32_t unit_end = unit_g + nst;
-      if (p.debug & 8) my_g = unit_end + (my_g & 1);  // MMA-only ablation: generators idle
+      if (OH_DEBUG(p) & 8) my_g = unit_end + (my_g & 1);  // MMA-only ablation: generators idle
       StageCodes<K> cur, nxt;
       if (my_g < unit_end) cur.load(row_saddr, sw, (int)(my_g - unit_g));
       uint32_t w[SP ? 32 : 64];
@@ -837,7 +842,7 @@ __global__ void __launch_bounds__(kOhThreads, 1)
           if (tr) OH_ACC(6, t0);
         }
         tc_fence_after();
-        if (!(p.debug & 4)) {
+        if (!(OH_DEBUG(p) & 4)) {
           OH_T0(t0);
           if constexpr (SP) {
             tmem_st32(lane_base + as * SC, w);
@@ -908,7 +913,7 @@ __global__ void __launch_bounds__(kOhThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty[acc]);
         }
-        if (p.debug & 1) continue;
+        if (OH_DEBUG(p) & 1) continue;
         constexpr int RC = 16 / DIGITS;  // real columns in this chunk
         const int mc = m_base + ch / DIGITS;  // first real column of the chunk
         const bool full_chunk = mc + RC <= p.M;
@@ -985,7 +990,7 @@ __global__ void __launch_bounds__(kOhThreads, 1)
           }
         }
       }
-      if (p.tma_out && p.out && !(p.debug & 1)) {
+      if (p.tma_out && p.out && !(OH_DEBUG(p) & 1)) {
         fence_proxy_async_smem();
         named_barrier_sync(1, 128);
         if (leader) {
@@ -1174,6 +1179,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     onehot_pair_kernel(const __grid_constant__ CUtensorMap codes_map, const __grid_constant__ CUtensorMap out_map,
                        const __grid_constant__ OneHotParams p) {
   static_assert(K >= 4, "K >= 4 on the tensor-core path");
+  static_assert(SP == 1 && KB == 4, "2:4-sparse one-hot, 4 K blocks (8 MMAs) per ring stage");
+  static_assert(FAST == 0 || FAST == 4 || FAST == 5 || FAST == 6, "epilogue variants: 0 generic, 4 / 5 / 6");
   constexpr int SC = SP ? (KB * kSparseStageCols) / 2 : kStageCols;  // TMEM columns per A ring stage
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window (LDS, not generic LD)
@@ -1217,7 +1224,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     for (int i = 0; i < p.a_stages; ++i) {
       // leader: its 4 generator warps + 1 forward from the peer's signaler;
       // peer: its 4 generator warps (collected locally, then forwarded)
-      mbar_init(&a_full[i], (leader && !(p.debug & 16)) ? 5 : 4);  // debug 16: leader ignores the peer
+      mbar_init(&a_full[i], (leader && !(OH_DEBUG(p) & 16)) ? 5 : 4);  // debug 16: leader ignores the peer
       mbar_init(&a_empty[i], 1);
     }
     fence_mbar_init();
@@ -1325,14 +1332,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     int sig_g = 0;
     while (walk.next(ntile, rt)) {
       for (int st = 0; st < nst; ++st) {
-        if (p.debug & 256)
+        if (OH_DEBUG(p) & 256)
           mbar_wait_crit(&a_full[as], aph, p.spin == 3 ? 1 : p.spin);
         else
           mbar_wait_rlx(&a_full[as], aph, p.spin == 3 ? 1 : p.spin);
         tc_fence_after();
         tc_fence_before();
-        if (lane == 0 && !(p.debug & 16)) {
-          if (p.debug & 256)
+        if (lane == 0 && !(OH_DEBUG(p) & 16)) {
+          if (OH_DEBUG(p) & 256)
             mbar_arrive_cluster(a_full_l + as * 8);
           else
             mbar_arrive_cluster_rlx(a_full_l + as * 8);
@@ -1366,7 +1373,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       int mma_g = 0, mma_unit = 0;
       bool next_ready = false;  // a_full of the stage at `as` already observed complete
       // launch parameters the per-stage path tests, read once into registers
-      const int dbg = p.debug, spin = p.spin, nkb = p.nkb, n_acc = p.n_acc;
+      const int dbg = OH_DEBUG(p), spin = p.spin, nkb = p.nkb, n_acc = p.n_acc;
       const bool watch = p.watch != 0;
       while (has_next) {
         ntile = nt_next;
@@ -1409,29 +1416,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           tc_fence_after();
           next_ready = false;
           if (!(dbg & 2)) {
-            if constexpr (SP && KB == 4) {
-              const uint64_t bst = b_desc0 + (uint64_t)((4 * st * NH * kKB) >> 4);
-              const uint32_t abase = a_col0 + as * SC;
-              issue_stage_sp<2>(d_tmem, abase, bst, bstep, idesc, st != 0, 4 * st + 1 < nkb, abase + 64);
-              // Probe the next ring stage while these 4 MMAs are queued: a blocking
-              // poll between stages (with the generators' tcgen05.st traffic on the
-              // SM) otherwise leaves the tensor pipe idle for ~100-200 cycles.
-              if (!(dbg & 2048) && !watch) {
-                const uint32_t as1 = as + 1 == nas ? 0 : as + 1;
-                next_ready = mbar_test_rlx(&a_full[as1], as + 1 == nas ? aph ^ 1 : aph);
-              }
-              if (4 * st + 2 < nkb)
-                issue_stage_sp<2>(d_tmem, abase + 32, bst + 2 * bstep, bstep, idesc, 1, 4 * st + 3 < nkb,
-                                  abase + 72);
-            } else if constexpr (SP && KB == 1)
-              issue_stage_sp1<2>(d_tmem, a_col0 + as * SC, b_desc0 + (uint64_t)((st * NH * kKB) >> 4), idesc, st != 0,
-                                 a_col0 + as * SC + 16);
-            else if constexpr (SP)
-              issue_stage_sp<2>(d_tmem, a_col0 + as * SC, b_desc0 + (uint64_t)((2 * st * NH * kKB) >> 4), bstep,
-                                idesc, st != 0, 2 * st + 1 < nkb, a_col0 + as * SC + 32);
-            else
-              issue_stage<2>(d_tmem, a_col0 + as * SC, b_desc0 + (uint64_t)((2 * st * NH * kKB) >> 4), bstep,
-                             idesc, st != 0, 2 * st + 1 < nkb);
+            const uint64_t bst = b_desc0 + (uint64_t)((4 * st * NH * kKB) >> 4);
+            const uint32_t abase = a_col0 + as * SC;
+            issue_stage_sp<2>(d_tmem, abase, bst, bstep, idesc, st != 0, 4 * st + 1 < nkb, abase + 64);
+            // Probe the next ring stage while these 4 MMAs are queued: a blocking
+            // poll between stages (with the generators' tcgen05.st traffic on the
+            // SM) otherwise leaves the tensor pipe idle for ~100-200 cycles.
+            if (!(dbg & 2048) && !watch) {
+              const uint32_t as1 = as + 1 == nas ? 0 : as + 1;
+              next_ready = mbar_test_rlx(&a_full[as1], as + 1 == nas ? aph ^ 1 : aph);
+            }
+            if (4 * st + 2 < nkb)
+              issue_stage_sp<2>(d_tmem, abase + 32, bst + 2 * bstep, bstep, idesc, 1, 4 * st + 3 < nkb, abase + 72);
           }
           commit_elect(&a_empty[as], true);
           if (lane == 0) TL(5, mma_g);
@@ -1468,97 +1464,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const int tslot = leader ? 0 : 8;
     while (walk.next(ntile, rt)) {
       {
-        long long t0 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
+        long long t0 = (OH_TRACE(p) && blockIdx.x < 2) ? clock64() : 0;
         mbar_wait(&code_full[cs], cphase);
-        if (tr && p.trace && blockIdx.x < 2 && lane == 0) atomicAdd(p.trace + 4 + tslot, (unsigned long long)(clock64() - t0));
+        if (tr && OH_TRACE(p) && blockIdx.x < 2 && lane == 0) atomicAdd(OH_TRACE(p) + 4 + tslot, (unsigned long long)(clock64() - t0));
       }
       const uint32_t row_saddr = smem_u32(code_smem + cs * code_tile_bytes) + row_in_tile * 128;
       const uint32_t unit_end = unit_g + nst;
-      if constexpr (SP && KB == 4) {
-        // 4 K blocks per stage, built and stored as two halves (register budget)
-        const int nsub = (p.nkb + 1) >> 1;
-        for (; my_g < unit_end; my_g += 2) {
-          const int st = (int)(my_g - unit_g);
-          StageCodes<K, 2> c0, c1;
-          const bool has1 = 2 * st + 1 < nsub;
-          c0.load(row_saddr, sw, 2 * st);
-          if (has1) c1.load(row_saddr, sw, 2 * st + 1);
-          uint32_t w[32], we[8];
-          build_sparse<K, 2>(c0, w, we);
-          if (lane == 0 && sub == 0) TL(0, my_g);
-          if (p.debug & 256)
-            mbar_wait_crit(&a_empty[as], aph ^ 1, p.spin == 3 ? 0 : p.spin);
-          else
-            mbar_wait_rlx(&a_empty[as], aph ^ 1, p.spin == 3 ? 0 : p.spin);
-          if (lane == 0 && sub == 0) TL(1, my_g);
-          tc_fence_after();
-          if (!(p.debug & 4)) {
-            tmem_st32(lane_base + as * SC, w);
-            tmem_st8(lane_base + as * SC + 64, we);
-          }
-          if (has1) {
-            build_sparse<K, 2>(c1, w, we);
-            if (!(p.debug & 4)) {
-              tmem_st32(lane_base + as * SC + 32, w);
-              tmem_st8(lane_base + as * SC + 72, we);
-            }
-          }
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&a_full[as]);
-          if (lane == 0 && sub == 0) TL(2, my_g);
-          as += 2;
-          if (as >= nas) {
-            as -= nas;
-            aph ^= 1;
-          }
-        }
-      } else {
-      StageCodes<K, KB == 4 ? 2 : KB> cur, nxt;
-      if (my_g < unit_end) cur.load(row_saddr, sw, (int)(my_g - unit_g));
-      uint32_t w[SP ? 16 * (KB == 4 ? 2 : KB) : 64];
-      uint32_t we[4 * (KB == 4 ? 2 : KB)];
+      // 4 K blocks per stage, built and stored as two halves (register budget)
+      const int nsub = (p.nkb + 1) >> 1;
       for (; my_g < unit_end; my_g += 2) {
         const int st = (int)(my_g - unit_g);
-        if (my_g + 2 < unit_end) nxt.load(row_saddr, sw, st + 2);
-        long long t0 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
-        if constexpr (SP)
-          build_sparse<K, KB == 4 ? 2 : KB>(cur, w, we);
+        StageCodes<K, 2> c0, c1;
+        const bool has1 = 2 * st + 1 < nsub;
+        c0.load(row_saddr, sw, 2 * st);
+        if (has1) c1.load(row_saddr, sw, 2 * st + 1);
+        uint32_t w[32], we[8];
+        build_sparse<K, 2>(c0, w, we);
+        if (lane == 0 && sub == 0) TL(0, my_g);
+        if (OH_DEBUG(p) & 256)
+          mbar_wait_crit(&a_empty[as], aph ^ 1, p.spin == 3 ? 0 : p.spin);
         else
-          build_onehot<K>(cur, w);
-        long long t1 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
-        mbar_wait_crit(&a_empty[as], aph ^ 1, p.spin == 3 ? 0 : p.spin);  // spin 3: only MMA/signaler poll
-        long long t2 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
+          mbar_wait_rlx(&a_empty[as], aph ^ 1, p.spin == 3 ? 0 : p.spin);
+        if (lane == 0 && sub == 0) TL(1, my_g);
         tc_fence_after();
-        if (!(p.debug & 4)) {
-          if constexpr (SP && KB == 1) {
-            tmem_st16(lane_base + as * SC, w);
-            tmem_st4(lane_base + as * SC + 16, we);
-          } else if constexpr (SP) {
-            tmem_st32(lane_base + as * SC, w);
-            tmem_st8(lane_base + as * SC + 32, we);
-          } else {
-            tmem_st64(lane_base + as * SC, w);
+        if (!(OH_DEBUG(p) & 4)) {
+          tmem_st32(lane_base + as * SC, w);
+          tmem_st8(lane_base + as * SC + 64, we);
+        }
+        if (has1) {
+          build_sparse<K, 2>(c1, w, we);
+          if (!(OH_DEBUG(p) & 4)) {
+            tmem_st32(lane_base + as * SC + 32, w);
+            tmem_st8(lane_base + as * SC + 72, we);
           }
-          tmem_st_wait();
         }
-        long long t3 = (p.trace && blockIdx.x < 2) ? clock64() : 0;
-        if (tr && p.trace && blockIdx.x < 2 && lane == 0) {
-          atomicAdd(p.trace + 5 + tslot, (unsigned long long)(t1 - t0));
-          atomicAdd(p.trace + 6 + tslot, (unsigned long long)(t2 - t1));
-          atomicAdd(p.trace + 7 + tslot, (unsigned long long)(t3 - t2));
-        }
+        tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&a_full[as]);  // local; the peer's signaler forwards it
-        cur = nxt;
+        if (lane == 0) mbar_arrive(&a_full[as]);
+        if (lane == 0 && sub == 0) TL(2, my_g);
         as += 2;
         if (as >= nas) {
           as -= nas;
           aph ^= 1;
         }
-      }
       }
       unit_g = unit_end;
       __syncwarp();
@@ -1582,7 +1531,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const int swz = ib == 32 ? (row_in_tile & 7) : ib == 16 ? ((row_in_tile >> 1) & 3) : ib == 8 ? ((row_in_tile >> 2) & 1) : 0;
     const float scale0 = (DIGITS == 1 && p.scales) ? __ldg(p.scales) : 1.0f;
     const uint64_t scale2 = pk_f2(scale0, scale0);
-    const bool etr = p.trace && blockIdx.x == 0 && warp == kPEpi0 && lane == 0;
+    const bool etr = OH_TRACE(p) && blockIdx.x == 0 && warp == kPEpi0 && lane == 0;
     const bool etl = warp == kPEpi0 && lane == 0;
     int epi_unit = 0;
     while (walk.next(ntile, rt)) {
@@ -1605,7 +1554,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         const int npass = HC / pc;
         long long e2 = etr ? clock64() : 0;
         long long e3 = e2;
-        if ((FAST == 4 || FAST == 6) && !(p.debug & 1)) {
+        if ((FAST == 4 || FAST == 6) && !(OH_DEBUG(p) & 1)) {
           // one thread per accumulator half stores the half's 128-row boxes: it waits
           // until its previous stores have read the slab, then releases the half
           if (sub == 0) {
@@ -1615,8 +1564,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           } else {
             named_barrier_sync(5 + 2 * hf, 128);
           }
-        } else if (!(p.debug & 1) && p.tma_out) {
-          if (lane == 0 && !(p.debug & 128)) bulk_wait_read0();  // this warp's single staging slab: previous store fully read
+        } else if (!(OH_DEBUG(p) & 1) && p.tma_out) {
+          if (lane == 0 && !(OH_DEBUG(p) & 128)) bulk_wait_read0();  // this warp's single staging slab: previous store fully read
           __syncwarp();
           if (etl) TL(11, epi_unit);
         }
@@ -1641,14 +1590,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           } else {
             named_barrier_sync(4, 256);
             if (elected) {
-              if (p.debug & 256)
+              if (OH_DEBUG(p) & 256)
                 mbar_arrive_cluster(acc_empty_l + acc * 8);
               else
                 mbar_arrive_cluster_rlx(acc_empty_l + acc * 8);
             }
           }
         }
-        if (p.debug & 1) continue;
+        if (OH_DEBUG(p) & 1) continue;
         if constexpr (FAST == 5) {
           // fp32 tables, 4 digit planes, no bias / act: 8 real columns of this pass,
           // exact int64 recombination, one f64 scale, into the swizzled staging slab
@@ -1672,62 +1621,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           }
           continue;
         }
-        if constexpr (FAST == 2) {
-          // 32 columns of this row straight to HBM: four 256-bit stores, each a
-          // full 32-byte sector (no staging, no proxy fence, no TMA queue)
-          if (live) {
-            float* dst = p.out + row * p.M + m_base + hf * HC + h2 * 32;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float f[8];
-#pragma unroll
-              for (int j = 0; j < 8; j += 2) {
-                const uint64_t b = pk_f2(__int_as_float(0x4B400000 + (int)v[8 * q + j]),
-                                         __int_as_float(0x4B400000 + (int)v[8 * q + j + 1]));
-                up_f2(mul_f2(add_f2(b, kNegMagic2), scale2), f[j], f[j + 1]);
-              }
-              asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + 8 * q), "f"(f[0]),
-                           "f"(f[1]), "f"(f[2]), "f"(f[3]), "f"(f[4]), "f"(f[5]), "f"(f[6]), "f"(f[7])
-                           : "memory");
-            }
-          }
-          continue;
-        }
-        if constexpr (FAST == 3) {
-          // 32 columns of this row into this warp's 32-row slice of the swizzled
-          // slab, then read back transposed (8 lanes per row) and written as
-          // full 128-byte lines with coalesced 16-byte stores
-          const uint32_t dst = out_saddr + (uint32_t)(h2 * (kRowsPerTile * 32 * 4));
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            float f0, f1, f2, f3;
-            const uint64_t b01 = pk_f2(__int_as_float(0x4B400000 + (int)v[4 * q]), __int_as_float(0x4B400000 + (int)v[4 * q + 1]));
-            const uint64_t b23 = pk_f2(__int_as_float(0x4B400000 + (int)v[4 * q + 2]), __int_as_float(0x4B400000 + (int)v[4 * q + 3]));
-            up_f2(mul_f2(add_f2(b01, kNegMagic2), scale2), f0, f1);
-            up_f2(mul_f2(add_f2(b23, kNegMagic2), scale2), f2, f3);
-            sts_v4(dst + (uint32_t)((q ^ swz) << 4), f0, f1, f2, f3);
-          }
-          __syncwarp();
-          const uint32_t slab = smem_u32(stage_out + hf * half_bytes) + (uint32_t)(h2 * (kRowsPerTile * 32 * 4)) +
-                                (uint32_t)(sub * 32 * 128);
-          const int c = lane & 7;
-          const int col = m_base + hf * HC + h2 * 32 + 4 * c;
-          const bool col_ok = col < p.M;  // M % 4 == 0: a 4-column chunk is wholly in or out
-          float* gbase = p.out + col;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int r = i * 4 + (lane >> 3);  // row inside this warp's slice
-            float4 x;
-            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
-                         : "r"(slab + (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4))));
-            const int64_t grow = row0 + sub * 32 + r;
-            if (grow < p.n && col_ok) *reinterpret_cast<float4*>(gbase + grow * p.M) = x;
-          }
-          __syncwarp();
-          continue;
-        }
-        if constexpr (FAST == 1 || FAST == 4 || FAST == 6) {
+        if constexpr (FAST == 4 || FAST == 6) {
           // 32 columns of this row: exact int -> f32, times the table scale,
           // into the 128B-swizzled staging slab (one 32-column box).
           // FAST 6 (the caller stacks): per-m-tile scale (scale_mtile % 32 == 0:
@@ -1857,8 +1751,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #pragma unroll
             for (int j = 0; j < RC; ++j) f[j] = apply_act(f[j], p.act);
           }
-          if (!p.out || (p.debug & 32)) {
-            if (p.debug & 32) {  // keep the math alive for the ablation
+          if (!p.out || (OH_DEBUG(p) & 32)) {
+            if (OH_DEBUG(p) & 32) {  // keep the math alive for the ablation
               float sacc = 0.f;
 #pragma unroll
               for (int j = 0; j < RC; ++j) sacc += f[j];
@@ -1896,7 +1790,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         }  // passes
         e3 = etr ? clock64() : 0;
         if (etl) TL(9, epi_unit);
-        if ((FAST == 4 || FAST == 6) && !(p.debug & 49)) {
+        if ((FAST == 4 || FAST == 6) && !(OH_DEBUG(p) & 49)) {
           fence_proxy_async_smem();
           if (sub != 0) {
             asm volatile("bar.arrive %0, 128;" ::"r"(6 + 2 * hf) : "memory");
@@ -1909,7 +1803,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
               bulk_commit();
             }
           }
-        } else if (p.tma_out && p.out && !(p.debug & 49)) {
+        } else if (p.tma_out && p.out && !(OH_DEBUG(p) & 49)) {
           fence_proxy_async_smem();
           __syncwarp();
           if (etl) TL(16, epi_unit);
@@ -1917,7 +1811,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             for (int bx = 0; bx < half_cols / ib; ++bx)
               tma_store_2d(&out_map, stage_out + hf * half_bytes + bx * (kRowsPerTile * ib * 4) + sub * 32 * (ib * 4),
                            m_base + hf * half_cols + bx * ib,
-                           (int32_t)(((p.debug & 64) ? (row0 & 2047) : row0) + sub * 32));  // 64: L2-resident rows
+                           (int32_t)(((OH_DEBUG(p) & 64) ? (row0 & 2047) : row0) + sub * 32));  // 64: L2-resident rows
             bulk_commit();
           }
         }
@@ -1927,10 +1821,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 
         if (etr) {
           const long long e4 = clock64();
-          atomicAdd(p.trace + 8, (unsigned long long)(e1 - e0));
-          atomicAdd(p.trace + 9, (unsigned long long)(e2 - e1));
-          atomicAdd(p.trace + 10, (unsigned long long)(e3 - e2));
-          atomicAdd(p.trace + 11, (unsigned long long)(e4 - e3));
+          atomicAdd(OH_TRACE(p) + 8, (unsigned long long)(e1 - e0));
+          atomicAdd(OH_TRACE(p) + 9, (unsigned long long)(e2 - e1));
+          atomicAdd(OH_TRACE(p) + 10, (unsigned long long)(e3 - e2));
+          atomicAdd(OH_TRACE(p) + 11, (unsigned long long)(e4 - e3));
         }
       }
       if (++acc == p.n_acc) {
@@ -2035,20 +1929,20 @@ static OneHotGeom onehot_geom(int C, int K, int M, int digits) {
   // the single-CTA kernel at N = 128 even when the image would fit (configs[1]/[3]
   // layers with C*K <= 1152: 79 -> 14 us for the FFN1 gather)
   int NT = 64;
-  if (const char* e = getenv("LUTGPU_OH_SINGLE128"))
+  if (const char* e = probe_env("LUTGPU_OH_SINGLE128"))
     if (e[0] == '1') NT = 128;
   while (NT > 16 && (size_t)NT * g.nkb * kKB > budget) NT /= 2;
   // do not waste B rows on a small M
   while (NT > 16 && NT / 2 >= M * digits) NT /= 2;
   {
-    const char* e = getenv("LUTGPU_OH_NT");  // tuning override (smaller only)
+    const char* e = probe_env("LUTGPU_OH_NT");  // tuning override (smaller only)
     if (e && atoi(e) >= 16 && atoi(e) < NT && (atoi(e) & 15) == 0) NT = atoi(e);
   }
   g.NT = NT;
   g.MT = NT / digits;
   g.ntiles = (M + g.MT - 1) / g.MT;
   // N <= 64 per SM leaves the i8 MMA issue-bound: pair two SMs (N = 2*NT)
-  const char* e = getenv("LUTGPU_OH_PAIR");
+  const char* e = probe_env("LUTGPU_OH_PAIR");
   g.pair = NT <= 64 && (NT >= 32 || digits == 1) && !(e && e[0] == '0');
   if (g.pair && (g.ntiles & 1)) ++g.ntiles;  // image tiles come in pairs (zero padded)
   g.img_bytes = (size_t)g.ntiles * NT * g.nkb * kKB;
@@ -2108,7 +2002,7 @@ const double* onehot_col_scale(const void* image, int C, int K, int M, int digit
 template <int K, int DIGITS>
 static int launch_onehot_k(const CUtensorMap& map, const CUtensorMap& omap, OneHotParams& p, size_t smem, int grid,
                            cudaStream_t stream) {
-  auto kern = p.sparse ? onehot_gemm_kernel<K, DIGITS, 1> : onehot_gemm_kernel<K, DIGITS, 0>;
+  auto kern = onehot_gemm_kernel<K, DIGITS, 1>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(onehot)");
   kern<<<grid, kOhThreads, smem, stream>>>(map, omap, p);
@@ -2120,16 +2014,10 @@ template <int K, int DIGITS>
 static int launch_pair_k(const CUtensorMap& map, const CUtensorMap& omap, OneHotParams& p, size_t smem, int grid,
                          cudaStream_t stream) {
   const int epi = DIGITS == 1 ? p.epi : (DIGITS == 4 && p.epi == 5) ? 5 : 0;
-  auto kern = !p.sparse            ? onehot_pair_kernel<K, DIGITS, 0, 2>
-              : p.stage_kb == 1 ? onehot_pair_kernel<K, DIGITS, 1, 1>
-              : p.stage_kb == 4 ? (epi == 5   ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 4 ? 5 : 0>
-                                   : epi == 1 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 1 : 0>
-                                   : epi == 2 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 2 : 0>
-                                   : epi == 3 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 3 : 0>
-                                   : epi == 4 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 4 : 0>
-                                   : epi == 6 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 6 : 0>
-                                              : onehot_pair_kernel<K, DIGITS, 1, 4>)
-                                : onehot_pair_kernel<K, DIGITS, 1, 2>;
+  auto kern = epi == 5   ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 4 ? 5 : 0>
+              : epi == 4 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 4 : 0>
+              : epi == 6 ? onehot_pair_kernel<K, DIGITS, 1, 4, DIGITS == 1 ? 6 : 0>
+                         : onehot_pair_kernel<K, DIGITS, 1, 4>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(onehot_pair)");
   kern<<<grid, kPairThreads, smem, stream>>>(map, omap, p);
@@ -2200,10 +2088,10 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
   p.out_hw = out_hw;
   p.out_i32 = out_i32;
   {
-    const char* dbg = getenv("LUTGPU_OH_DEBUG");
+    const char* dbg = probe_env("LUTGPU_OH_DEBUG");
     p.debug = dbg ? atoi(dbg) : 0;
   }
-  const char* pair_env = getenv("LUTGPU_OH_PAIR");
+  const char* pair_env = probe_env("LUTGPU_OH_PAIR");
   if (g.pair && !(pair_env && pair_env[0] == '0')) {
     // ---------------- CTA-pair kernel: MMA N = 2*NT, 256-row pair tiles
     const int NN = 2 * g.NT;
@@ -2213,19 +2101,19 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
     p.n_acc = 2;
     p.spin = 3;  // MMA issuer and peer signaler poll their critical barriers; generators sleep
     {
-      const char* e1 = getenv("LUTGPU_OH_ACC1");
+      const char* e1 = probe_env("LUTGPU_OH_ACC1");
       if (e1 && e1[0] == '1') p.n_acc = 1;
-      const char* e2 = getenv("LUTGPU_OH_SPIN");
+      const char* e2 = probe_env("LUTGPU_OH_SPIN");
       if (e2) p.spin = atoi(e2);
     }
     {
-      const char* e3 = getenv("LUTGPU_OH_DENSE");
+      const char* e3 = probe_env("LUTGPU_OH_DENSE");
       p.sparse = (e3 && e3[0] == '1') ? 0 : 1;
     }
     p.stage_kb = 4;  // 4 K blocks (8 sparse MMAs) per ring handshake
-    p.watch = !(getenv("LUTGPU_OH_WATCH") && getenv("LUTGPU_OH_WATCH")[0] == '0');
+    p.watch = !(probe_env("LUTGPU_OH_WATCH") && probe_env("LUTGPU_OH_WATCH")[0] == '0');
     {
-      const char* e4 = getenv("LUTGPU_OH_KB");
+      const char* e4 = probe_env("LUTGPU_OH_KB");
       if (e4 && (e4[0] == '1' || e4[0] == '2' || e4[0] == '4')) p.stage_kb = e4[0] - '0';
     }
     const int sc = p.sparse ? (p.stage_kb * kSparseStageCols) / 2 : kStageCols;
@@ -2266,20 +2154,20 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
                        scale_mtile == 0 && out_hw == 0 && g.NT == 64 && !(p.debug & 512);
     int epi = plain ? 4 : 0;
     if (plain) {
-      if (const char* e = getenv("LUTGPU_OH_EPI")) epi = atoi(e);
+      if (const char* e = probe_env("LUTGPU_OH_EPI")) epi = atoi(e);
       if (epi < 0 || epi > 4) epi = 4;
     }
     // int8 caller stacks (bias / GELU / ReLU / per-m-tile scales, the BERT and FFN
     // layers): compile-time variant of the same per-half TMA-store epilogue
     if (!plain && digits == 1 && p.sparse && p.stage_kb == 4 && out && !out_i32 && out_hw == 0 && g.NT == 64 &&
         !(p.debug & 512) && (scale_mtile == 0 || scale_mtile % 32 == 0) &&
-        (reinterpret_cast<uintptr_t>(bias) & 15) == 0 && !(getenv("LUTGPU_OH_EPI") && atoi(getenv("LUTGPU_OH_EPI")) == 0))
+        (reinterpret_cast<uintptr_t>(bias) & 15) == 0 && !(probe_env("LUTGPU_OH_EPI") && atoi(probe_env("LUTGPU_OH_EPI")) == 0))
       epi = 6;
     // plain fp32 (4 digit planes): compile-time recombination epilogue, per-warp TMA stores
     if (digits == 4 && p.sparse && p.stage_kb == 4 && out && !out_i32 && !bias && !act && out_hw == 0 &&
-        g.NT == 64 && !(p.debug & 512) && !(getenv("LUTGPU_OH_EPI") && atoi(getenv("LUTGPU_OH_EPI")) == 0))
+        g.NT == 64 && !(p.debug & 512) && !(probe_env("LUTGPU_OH_EPI") && atoi(probe_env("LUTGPU_OH_EPI")) == 0))
       epi = 5;
-    const char* e5 = getenv("LUTGPU_OH_TMAOUT");
+    const char* e5 = probe_env("LUTGPU_OH_TMAOUT");
     if (!(e5 && e5[0] == '0') && out && out_hw == 0 && (M % 4) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
         ib >= 4 && half_cols % ib == 0 && base_smem + stage_bytes <= max_smem_optin()) {
       if (make_tmap_2d_f32_box(&omap, out, (uint64_t)M, (uint64_t)n, (uint32_t)ib, (epi == 4 || epi == 6) ? kRowsPerTile : 32)) {
@@ -2299,7 +2187,7 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
     const size_t smem = base_smem + (p.stage_slab ? stage_bytes : 0);
     p.trace = nullptr;
     p.tl = nullptr;
-    const char* tl_path = getenv("LUTGPU_OH_TL");
+    const char* tl_path = probe_env("LUTGPU_OH_TL");
     if (tl_path) {
       cudaMalloc(&p.tl, 2 * kTlEv * kTlN * sizeof(unsigned long long));
       cudaMemsetAsync(p.tl, 0, 2 * kTlEv * kTlN * sizeof(unsigned long long), stream);
@@ -2324,7 +2212,7 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
         cudaFree(t);
       }
     } tld{p.tl, stream, tl_path};
-    if (getenv("LUTGPU_OH_TRACE")) {
+    if (probe_env("LUTGPU_OH_TRACE")) {
       cudaMalloc(&p.trace, 16 * sizeof(unsigned long long));
       cudaMemsetAsync(p.trace, 0, 16 * sizeof(unsigned long long), stream);
     }
@@ -2357,7 +2245,7 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
   // TMEM: 2 accumulators (2*NT columns) + the A ring (64 dense / 40 sparse columns per stage);
   // an even ring depth (the two generator warp groups own alternate stages)
   {
-    const char* e3 = getenv("LUTGPU_OH_DENSE");
+    const char* e3 = probe_env("LUTGPU_OH_DENSE");
     p.sparse = (e3 && e3[0] == '1') ? 0 : 1;
   }
   const int sc1 = p.sparse ? kSparseStageCols : kStageCols;
@@ -2365,7 +2253,7 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
   if (p.a_stages > kMaxAStages) p.a_stages = kMaxAStages;
   if (p.a_stages < 2) return fail(LUT_ERR_CONFIG, "one-hot gather: TMEM budget exceeded");
   {
-    const char* st = getenv("LUTGPU_OH_ASTAGES");
+    const char* st = probe_env("LUTGPU_OH_ASTAGES");
     if (st && atoi(st) >= 2 && atoi(st) <= p.a_stages) p.a_stages = atoi(st);
   }
   uint32_t cols = 2 * g.NT + p.a_stages * sc1;
@@ -2373,7 +2261,7 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
   while (alloc < cols) alloc <<= 1;
   p.tmem_cols = alloc;
   {
-    const char* dbg = getenv("LUTGPU_OH_DEBUG");
+    const char* dbg = probe_env("LUTGPU_OH_DEBUG");
     p.debug = dbg ? atoi(dbg) : 0;
   }
   const int nsm = num_sms();
@@ -2406,7 +2294,7 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
   }
   const size_t smem = base_smem + (p.tma_out ? stage_bytes : 0);
   unsigned long long* trace = nullptr;
-  if (getenv("LUTGPU_OH_TRACE")) {
+  if (probe_env("LUTGPU_OH_TRACE")) {
     cudaMalloc(&trace, 16 * sizeof(unsigned long long));
     cudaMemsetAsync(trace, 0, 16 * sizeof(unsigned long long), stream);
   }

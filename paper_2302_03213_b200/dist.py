@@ -29,6 +29,8 @@ def shard_sizes(n: int, world: int) -> list[int]:
 
 def gather_rows(local: torch.Tensor, n_total: int, group=None) -> torch.Tensor:
     """All-gather row shards (uneven allowed) into the full (n_total, ...) tensor."""
+    if local.is_cuda and dist.get_backend(group) == "gloo":  # gloo moves host tensors only
+        return gather_rows(local.cpu(), n_total, group).to(local.device)
     world = dist.get_world_size(group)
     sizes = shard_sizes(n_total, world)
     rank = dist.get_rank(group)

@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import weakref
+import zlib
 
 import numpy as np
 import torch
@@ -81,7 +82,8 @@ class LutLayer:
                                         scale=qtable.scales_tensor(self.device) if isinstance(qtable, LookupTableI8)
                                         else torch.as_tensor(np.asarray(qtable.scale, F32).reshape(-1),
                                                              device=self.device),
-                                        scale_mtile=getattr(qtable, "scale_mtile", 0))
+                                        scale_mtile=getattr(qtable, "scale_mtile", 0),
+                                        validated=isinstance(qtable, LookupTableI8))
         if self.table is None and self.qtable is None:
             self.rebuild()
         m = self.m
@@ -165,6 +167,7 @@ class LutLayer:
             twin.__dict__.update({k: v for k, v in self.__dict__.items() if k != "_act_twins"})
             twin.act = act
             twin._desc_cache = {}
+            twin._pipelines = {}  # own executor handles: their finalizer is tied to the twin
             cache[act] = twin
         return twin
 
@@ -258,10 +261,15 @@ class LutLayer:
             elif out.shape != (n, self.m) or out.dtype != F32 or not out.flags.c_contiguous:
                 raise ShapeError(f"out must be a contiguous f32 array of shape {(n, self.m)}")
             chunk = max(1, min(n, PIPELINE_CHUNK_BYTES // max(1, 4 * max(self.d, self.m))))
+            # the descriptor may launch one-time prep work (table image) on torch's
+            # stream: build it first, then sync, since the executor runs on its own
+            # non-blocking streams
+            desc = self.desc(integer)
+            pipe = self._pipeline(chunk)
             torch.cuda.current_stream().synchronize()
             near = C.c_int32(0)
-            check(load().lut_pipeline_run(self._pipeline(chunk), C.byref(self.desc(integer)),
-                                          a_h.ctypes.data, n, out.ctypes.data, C.byref(near)), "lut_layer_infer")
+            check(load().lut_pipeline_run(pipe, C.byref(desc), a_h.ctypes.data, n, out.ctypes.data, C.byref(near)),
+                  "lut_layer_infer")
             EncodeStats.last_near_ties = near.value
             return out
         a_dev = D.to_device(a, F32, self.device)
@@ -279,26 +287,68 @@ class LutLayer:
         kind = D.kind_of(a)
         codes = encode_hash(D.to_device(a, F32, self.device), self.trees)
         act = ACTS[self.act]
+        # leaves are data: a code >= K raises CorruptionError like lut_gather_i32 /
+        # lut_matmul_ref (kernels.py:117-118, pq.py:209-210), never a clamp
+        err = D.ErrFlag(self.device)
         if integer:
             out = _gather_i8_f32(codes, self.qtable.q, self.qtable.scales_tensor(self.device), self.qtable.scale_mtile,
-                                 self.bias, act, self.c, self.k, self.m)
+                                 self.bias, act, self.c, self.k, self.m, err.p)
         else:
-            out = _gather_f32(codes, self.table, self.bias, act, self.c, self.k, self.m)
+            out = _gather_f32(codes, self.table, self.bias, act, self.c, self.k, self.m, err.p)
+        check(load().lut_read_status(err.p, D.stream_ptr()), "lut_layer_infer")
         return D.from_device(out, kind)
 
 
-_FOREIGN: dict[int, tuple] = {}
+_FOREIGN = weakref.WeakKeyDictionary()   # reference layer -> (fingerprint, device layer)
+_FOREIGN_BY_ID: dict[int, tuple] = {}     # layers that cannot be weak-referenced (bounded)
+_FOREIGN_BY_ID_MAX = 8
+
+
+def _content_key(x):
+    """Cheap identity of a host array's contents: the reference SGD step
+    updates books and bias in place (train.py:162), so those are checksummed;
+    tables are rebuilt as new objects (softpq.py:125-132), so identity suffices."""
+    if x is None:
+        return None
+    if isinstance(x, torch.Tensor):
+        return ("t", x.data_ptr(), x._version, tuple(x.shape))
+    a = np.ascontiguousarray(x)
+    return ("a", a.dtype.str, a.shape, zlib.crc32(a.view(np.uint8).reshape(-1)))
+
+
+def _fingerprint(layer) -> tuple:
+    qt = getattr(layer, "qtable", None)
+    return (_content_key(layer.books), _content_key(layer.bias), _sample_key(getattr(layer, "table", None)),
+            None if qt is None else (_sample_key(qt.q), float(np.asarray(qt.scale).reshape(-1)[0])))
+
+
+def _sample_key(x):
+    """Object identity plus a checksum of ~4096 strided entries (a table that
+    was replaced by a new object of the same id still changes the key)."""
+    if x is None:
+        return None
+    if isinstance(x, torch.Tensor):
+        return _content_key(x)
+    a = np.asarray(x).reshape(-1)
+    step = max(1, a.size // 4096)
+    return (id(x), a.dtype.str, a.size, zlib.crc32(np.ascontiguousarray(a[::step]).view(np.uint8)))
 
 
 def as_device_layer(layer) -> LutLayer:
-    """Our LutLayer as is; a reference-style layer converted once (cached
-    while its arrays are the same objects)."""
+    """Our LutLayer as is; a reference-style layer is converted once and the
+    device copy reused while its books / bias contents and its table objects
+    are unchanged (an in-place update of books or bias re-converts).  The cache
+    holds the reference layer weakly, so dropping it frees the HBM tables."""
     if isinstance(layer, LutLayer):
         return layer
-    key = id(layer)
-    arrays = (layer.books, getattr(layer, "table", None), getattr(layer, "qtable", None), layer.bias)
-    hit = _FOREIGN.get(key)
-    if hit is not None and all(x is y for x, y in zip(hit[0], arrays)):
+    fp = _fingerprint(layer)
+    try:
+        hit = _FOREIGN.get(layer)
+        weak = True
+    except TypeError:
+        hit = _FOREIGN_BY_ID.get(id(layer))
+        weak = False
+    if hit is not None and hit[0] == fp:
         return hit[1]
     qt = getattr(layer, "qtable", None)
     if qt is not None and not isinstance(qt, LookupTableI8):
@@ -307,5 +357,10 @@ def as_device_layer(layer) -> LutLayer:
         v=int(layer.cfg.v), k=int(layer.cfg.k))
     dl = LutLayer(cfg=cfg, books=layer.books, weight=None, bias=layer.bias, table=getattr(layer, "table", None),
                   qtable=qt, trees=getattr(layer, "trees", None))
-    _FOREIGN[key] = (arrays, dl)
+    if weak:
+        _FOREIGN[layer] = (fp, dl)
+    else:
+        if len(_FOREIGN_BY_ID) >= _FOREIGN_BY_ID_MAX:
+            _FOREIGN_BY_ID.pop(next(iter(_FOREIGN_BY_ID)))
+        _FOREIGN_BY_ID[id(layer)] = (fp, dl)
     return dl

@@ -16,7 +16,7 @@ import torch
 
 from . import _device as D
 from ._lib import check, load
-from .errors import ShapeError
+from .errors import ConfigError, ShapeError
 from .kernels import ACTS, EncodeStats, KernelPlan, _gather_f32, _gather_i8_f32, lut_layer_infer
 from .layer import LutLayer, as_device_layer
 from .tensor import conv_out_hw
@@ -66,6 +66,8 @@ def conv_forward(x, lut: LutLayer, cin: int, kernel: int, stride: int, pad: int,
         raise ShapeError(f"patch cols {cin * kernel * kernel} != C*V = {lut.d}")
     if integer is None:
         integer = lut.has_qtable
+    if integer and not lut.has_qtable:  # kernels.py:166-170
+        raise ConfigError("integer path requested but the layer has no quantized table")
     kind = D.kind_of(x)
     dev = lut.device
     x_dev = D.to_device(x, F32, dev)
@@ -77,11 +79,24 @@ def conv_forward(x, lut: LutLayer, cin: int, kernel: int, stride: int, pad: int,
                                   lut.c, lut.k, lut.v, D.ptr(codes), 8, D.ptr(near), D.stream_ptr()), "LutConv")
     out = torch.empty((b, lut.m, ho, wo), dtype=torch.float32, device=dev)
     act = ACTS[lut.act]
-    if integer:
-        _gather_i8_f32(codes, lut.qtable.q, lut.qtable.scales_tensor(dev), lut.qtable.scale_mtile, lut.bias, act,
-                       lut.c, lut.k, lut.m, None, out_hw=ho * wo, out=out)
+    if lut.uses_tensor_cores(bool(integer)):
+        # the one-hot gather TMA-loads 16-byte code rows: pad the (n, C) codes
+        stride_c = lut.code_stride
+        padded = torch.zeros((n, stride_c), dtype=torch.uint8, device=dev)
+        padded[:, :lut.c] = codes
+        desc = lut.desc(bool(integer))
+        check(lib.lut_gather_onehot(D.ptr(padded), stride_c, n, lut.c, lut.k, lut.m, desc.onehot_digits,
+                                    desc.onehot_image, desc.scales if integer else None,
+                                    lut.qtable.scale_mtile if integer else 0, D.ptr(lut.bias), act, D.ptr(out),
+                                    None, ho * wo, D.stream_ptr()), "LutConv")
     else:
-        _gather_f32(codes, lut.table, lut.bias, act, lut.c, lut.k, lut.m, None, out_hw=ho * wo, out=out)
+        err = D.ErrFlag(dev)
+        if integer:
+            _gather_i8_f32(codes, lut.qtable.q, lut.qtable.scales_tensor(dev), lut.qtable.scale_mtile, lut.bias,
+                           act, lut.c, lut.k, lut.m, err.p, out_hw=ho * wo, out=out)
+        else:
+            _gather_f32(codes, lut.table, lut.bias, act, lut.c, lut.k, lut.m, err.p, out_hw=ho * wo, out=out)
+        check(lib.lut_read_status(err.p, D.stream_ptr()), "LutConv")
     return D.from_device(out, kind)
 
 

@@ -8,7 +8,7 @@ reference rejects per-codebook scales)."""
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -28,6 +28,10 @@ class LookupTableI8:
     q: object             # np.ndarray int8 or torch int8 tensor
     scale: object         # np.float32, or 1-D array of per-m-tile scales
     scale_mtile: int = 0  # 0 = one scale per table (reference)
+    # set by quantize_table: entries and scales were produced by the device
+    # quantizer (never -128, scales > 0), so construction skips the value
+    # checks and their device->host sync
+    validated: bool = field(default=False, compare=False, repr=False)
 
     def __post_init__(self) -> None:
         q = self.q
@@ -38,6 +42,8 @@ class LookupTableI8:
         if not ok:
             raise ShapeError(f"quantized table must be int8 (C, K, M), got {getattr(q, 'dtype', None)} "
                              f"{tuple(q.shape)}")
+        if self.validated:
+            return
         s = self.scale
         svals = s.detach().cpu().numpy() if isinstance(s, torch.Tensor) else np.asarray(s, F32)
         if not np.all(svals > 0):
@@ -76,10 +82,10 @@ def quantize_table(table, scale_mtile: int = 0) -> LookupTableI8:
                                  err.p, D.stream_ptr()), "quantize_table")
     check(lib.lut_read_status(err.p, D.stream_ptr()), "quantize_table")
     if kind == D.TORCH_CUDA:
-        return LookupTableI8(q=q, scale=scales if scale_mtile else scales[0], scale_mtile=scale_mtile)
+        return LookupTableI8(q=q, scale=scales if scale_mtile else scales[0], scale_mtile=scale_mtile, validated=True)
     qh = D.from_device(q, kind)
     sh = scales.cpu().numpy()
-    return LookupTableI8(q=qh, scale=sh if scale_mtile else F32(sh[0]), scale_mtile=scale_mtile)
+    return LookupTableI8(q=qh, scale=sh if scale_mtile else F32(sh[0]), scale_mtile=scale_mtile, validated=True)
 
 
 def dequantize(qt: LookupTableI8):

@@ -158,3 +158,71 @@ def test_gather_rows_gloo_world2(n):
         p.join(120)
     res = dict(q.get(timeout=10) for _ in range(2))
     assert res == {0: True, 1: True}
+
+
+class _HostLayer:
+    """Stand-in with LutLayer.forward_device's contract for the CPU test: a
+    row-wise map (out row i depends only on input row i), as the LUT layer is."""
+
+    def forward_device(self, a, integer):
+        import torch
+
+        w = torch.arange(a.shape[1] * 5, dtype=torch.float32).reshape(a.shape[1], 5) / 7.0
+        return a @ w + (1.0 if integer else 0.0)
+
+
+def _sharded_worker(rank, world, port, n, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2302_03213_b200.dist import shard_range, sharded_forward
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        full = torch.linspace(-3, 3, n * 4, dtype=torch.float32).reshape(n, 4)
+        s, e = shard_range(n, rank, world)
+        layer = _HostLayer()
+        got = sharded_forward(full[s:e], layer, True, n_total=None, gather=True)  # n_total via all_reduce
+        local = sharded_forward(full[s:e], layer, False)
+        q.put((rank, bool(torch.equal(got, layer.forward_device(full, True))) and local.shape[0] == e - s))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [9, 2])
+def test_sharded_forward_gloo_world2(n):
+    import multiprocessing as mp
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    res = dict(q.get(timeout=10) for _ in range(2))
+    assert res == {0: True, 1: True}
+
+
+def test_bench_reference_arm_small():
+    """bench.py --impl reference on a small layer: one JSON line with the
+    reference-arm keys (all-core value, one-core figure, linearity check)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--dim", "256",
+                        "--v", "16", "--cpu-rows", "64", "--steps", "2", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["steps"] == 2 and line["warmup"] == 1
+    assert line["one_core"]["cores"] == 1 and "linear" in line["linearity"]
+    assert line["config"]["rows_sampled_per_step"] == line["cpu_baseline"]["cores"] * 64
+    assert line["e2e"]["h2d_bytes_per_step"] == 0

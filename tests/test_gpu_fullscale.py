@@ -1,0 +1,112 @@
+"""GPU: configs[4] at full scale (BASELINE.json configs[4]: N = 2^20 rows,
+D = M = 4096, V = 32 -> C = 128, K in {16, 64}).
+
+* Every one of the 2^20 x 128 codes of the benched encode is compared with an
+  independent f64 argmin of the literal distances sum_j (a_j - p_j)^2
+  (pq.py:53-73, argmin ties -> lowest k, pq.py:171-174), computed with torch
+  in f64 on the device in row chunks.  The north-star near-tie count (f64
+  relative gap between best and second best < 1e-6) is computed on the way.
+* A stratified 2^16-row sample is compared with the oracle's encode_hard.
+* The int8 layer output at the benched K = 64 geometry (C = 128, M = 4096)
+  is compared byte for byte with the oracle (kernels.py:105-135, 143-178).
+"""
+
+import multiprocessing as mp
+
+import numpy as np
+import pytest
+
+from oracle import lut_oracle as O
+
+pytestmark = pytest.mark.gpu
+F32 = np.float32
+N_FULL = 1 << 20
+D_FULL = 4096
+V = 32
+C = D_FULL // V
+
+
+@pytest.fixture(scope="module")
+def L():
+    import paper_2302_03213_b200 as lg
+
+    return lg
+
+
+def f64_literal_argmin(a_dev, books_dev, chunk):
+    """(codes u8 (N, C), near_tie_1e6 count, min relative gap) from literal
+    f64 distances; torch.argmin returns the first minimum (lowest k)."""
+    import torch
+
+    n = a_dev.shape[0]
+    c, k, v = books_dev.shape
+    p64 = books_dev.double()[None]  # (1, C, K, V)
+    codes = torch.empty((n, c), dtype=torch.uint8, device=a_dev.device)
+    near = 0
+    for r0 in range(0, n, chunk):
+        r1 = min(n, r0 + chunk)
+        d = torch.sub(a_dev[r0:r1].double().view(r1 - r0, c, 1, v), p64).square_().sum(-1)  # (rows, C, K)
+        codes[r0:r1] = d.argmin(-1).to(torch.uint8)
+        two = d.topk(2, dim=-1, largest=False).values
+        gap = (two[..., 1] - two[..., 0]) / torch.clamp(torch.maximum(two[..., 0].abs(), two[..., 1].abs()),
+                                                      min=1e-300)
+        near += int((gap < 1e-6).sum())
+        del d, two, gap
+    return codes, near
+
+
+def _hard_chunk(args):
+    a, books = args
+    return O.encode_hard(a, books)
+
+
+def oracle_encode_hard(a, books, workers=8):
+    """encode_hard over row chunks on the host cores (fork pool)."""
+    parts = [(a[i:i + 1024], books) for i in range(0, a.shape[0], 1024)]
+    with mp.get_context("fork").Pool(min(workers, mp.cpu_count())) as pool:
+        return np.concatenate(pool.map(_hard_chunk, parts))
+
+
+@pytest.mark.parametrize("k", [16, 64])
+def test_fullscale_codes_vs_f64(L, k):
+    import torch
+
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(1234)
+    books = torch.randn((C, k, V), generator=g, device=dev)
+    ga = torch.Generator(device=dev).manual_seed(99)
+    a = torch.randn((N_FULL, D_FULL), generator=ga, device=dev)
+    lib = L._lib.load()
+    prep = L.kernels.prepare_books(books)
+    stride = int(lib.lut_code_stride(C))
+    codes = torch.empty((N_FULL, stride), dtype=torch.uint8, device=dev)
+    near_redecided = torch.zeros(1, dtype=torch.int32, device=dev)
+    L._lib.check(lib.lut_encode_f32(a.data_ptr(), N_FULL, D_FULL, prep.data_ptr(), C, k, V, codes.data_ptr(), 8,
+                                    stride, near_redecided.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    want, near_1e6 = f64_literal_argmin(a, books, chunk=2048 if k == 16 else 512)
+    got = codes[:, :C]
+    mism = int((got != want).sum())
+    print(f"K={k}: {N_FULL * C} codes, mismatches {mism}, near ties (f64 gap < 1e-6) {near_1e6}, "
+          f"f64 re-decisions {int(near_redecided.item())}")
+    assert mism == 0
+    # stratified sample (every 16th row) against the oracle's encode_hard
+    idx = torch.arange(0, N_FULL, 16, device=dev)
+    a_s = a[idx].cpu().numpy()
+    ref = oracle_encode_hard(a_s, books.cpu().numpy())
+    np.testing.assert_array_equal(got[idx].cpu().numpy(), ref)
+
+
+def test_k64_int8_layer_bytes_at_benched_geometry(L):
+    """configs[4], K = 64, int8 tables, tensor-core gather at C = 128,
+    M = 4096 (the benched kernels), 4096 rows: bytes equal to the oracle."""
+    rng = O.make_rng(64)
+    n, k, m = 4096, 64, 4096
+    books = rng.standard_normal((C, k, V)).astype(F32)
+    w = (rng.standard_normal((D_FULL, m)) / np.sqrt(D_FULL)).astype(F32)
+    a = rng.standard_normal((n, D_FULL)).astype(F32)
+    layer = L.LutLayer(cfg=L.PqConfig(v=V, k=k), books=books, weight=w, qat=True, gather="tensor")
+    assert layer.uses_tensor_cores(True)
+    got = L.lut_layer_infer(a, layer, integer=True)
+    q, s = O.quantize_table(O.build_table(w, books))
+    want = O.lut_layer_infer(a, books, q=q, scale=s)
+    assert got.tobytes() == want.tobytes()
