@@ -151,6 +151,15 @@ LUT_API int lut_gather_i8(const uint8_t* codes, int32_t code_bits, int64_t n, in
 LUT_API int lut_build_table_f32(const float* b, int32_t m, const float* books, int32_t c, int32_t k,
                         int32_t v, float* table, lut_stream_t stream);
 
+/*
+ * Dense reference product (tensor.py:110-125, matmul_ref): out (n, m) =
+ * a (n, d) @ b (d, m), each product rounded to f32 and added in ascending k
+ * from +0.0 (no FMA) -- bitwise equal to the reference.  The dense baseline of
+ * bench_kernel (kernels.py:288-349), not part of the LUT path.
+ */
+LUT_API int lut_matmul_ref_f32(const float* a, const float* b, int64_t n, int32_t d, int32_t m, float* out,
+                               lut_stream_t stream);
+
 /* Bytes of scratch for lut_quantize_table(). */
 LUT_API size_t lut_quantize_scratch_bytes(int32_t c, int32_t k, int32_t m, int32_t scale_mtile);
 

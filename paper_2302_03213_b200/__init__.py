@@ -19,8 +19,10 @@ from .errors import (
 )
 from .kernels import (
     MAX_GROUP,
+    BenchReport,
     EncodeStats,
     KernelPlan,
+    bench_kernel,
     centroid_search_fast,
     encode_hash,
     flop_counter,
@@ -31,7 +33,8 @@ from .kernels import (
 )
 from .quant import QMAX, LookupTableI8, dequantize, quantize_table
 from .pq import PqConfig, build_table, encode_hard, lut_matmul_ref, pq_amm, validate_codebooks
-from .tensor import as_matrix, im2col
+from .tensor import as_matrix, im2col, matmul_ref, split_subvectors
+from .rng import child_rng, make_rng
 from .layer import LutLayer, as_device_layer
 from .nn import Conv, Dense, LutConv, LutConv2d, LutDense, LutLinear, Model, Relu, predict_fast
 from .container import load_model, model_bytes, model_from_bytes, save_model

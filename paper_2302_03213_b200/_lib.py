@@ -51,6 +51,7 @@ SIGNATURES = {
     "lut_gather_f32": (C.c_int, [P, I32, I64, I32, I32, I32, P, P, I32, P, I64, P, P]),
     "lut_gather_i8": (C.c_int, [P, I32, I64, I32, I32, I32, P, P, I32, P, I32, P, P, I64, P, P]),
     "lut_build_table_f32": (C.c_int, [P, I32, P, I32, I32, I32, P, P]),
+    "lut_matmul_ref_f32": (C.c_int, [P, P, I64, I32, I32, P, P]),
     "lut_quantize_scratch_bytes": (C.c_size_t, [I32, I32, I32, I32]),
     "lut_quantize_table": (C.c_int, [P, I32, I32, I32, I32, P, P, P, P, P]),
     "lut_read_status": (C.c_int, [P, P]),

@@ -61,6 +61,7 @@ int gather_i8_strided(const uint8_t* codes, int code_bits, int64_t code_stride, 
 int build_table(const float* b, int M, const float* books, int C, int K, int V, float* table,
                 cudaStream_t stream);
 size_t quantize_scratch_bytes(int C, int K, int M, int mtile);
+int matmul_ref(const float* a, const float* b, int64_t n, int d, int m, float* out, cudaStream_t stream);
 int quantize_table(const float* t, int C, int K, int M, int mtile, int8_t* q, float* scales, void* scratch,
                    int* err, cudaStream_t stream);
 
@@ -297,6 +298,13 @@ int lut_build_table_f32(const float* b, int32_t m, const float* books, int32_t c
   if (m < 0) return fail(LUT_ERR_CONFIG, "negative m");
   if ((int64_t)c * k * m > 0 && (!b || !books || !table)) return fail(LUT_ERR_CONFIG, "null pointer");
   return build_table(b, m, books, c, k, v, table, (cudaStream_t)stream);
+}
+
+int lut_matmul_ref_f32(const float* a, const float* b, int64_t n, int32_t d, int32_t m, float* out,
+                       lut_stream_t stream) {
+  if (n < 0 || d < 0 || m < 0) return fail(LUT_ERR_CONFIG, "negative size");
+  if (n > 0 && m > 0 && (!out || (d > 0 && (!a || !b)))) return fail(LUT_ERR_CONFIG, "null pointer");
+  return matmul_ref(a, b, n, d, m, out, (cudaStream_t)stream);
 }
 
 size_t lut_quantize_scratch_bytes(int32_t c, int32_t k, int32_t m, int32_t scale_mtile) {

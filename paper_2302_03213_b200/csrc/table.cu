@@ -107,4 +107,59 @@ int quantize_table(const float* t, int C, int K, int M, int mtile, int8_t* q, fl
   return LUT_OK;
 }
 
+// Dense reference product (tensor.py:110-125, matmul_ref): out[n,m] =
+// sum_k a[n,k]*b[k,m] with each product rounded to f32 and added in ascending
+// k from +0.0 (numpy's `out += a[:, k:k+1] * b[k:k+1, :]`, no FMA).  Not on the
+// LUT path: it is the dense baseline bench_kernel times the LUT layer against.
+// 64 x 64 output tile per CTA, 256 threads x (4 rows x 4 cols), k staged
+// through SMEM 16 at a time.
+__global__ void __launch_bounds__(256) matmul_ref_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                                         int N, int D, int M, float* __restrict__ out) {
+  __shared__ float as[16][64 + 1];
+  __shared__ float bs[16][64];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t row0 = (int64_t)blockIdx.y * 64, col0 = (int64_t)blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < D; k0 += 16) {
+    for (int i = threadIdx.x; i < 16 * 64; i += 256) {
+      const int kk = i & 15, r = i >> 4;  // a tile: 64 rows x 16 k
+      const int64_t gr = row0 + r;
+      as[kk][r] = (gr < N && k0 + kk < D) ? __ldg(a + gr * D + k0 + kk) : 0.0f;
+      const int cc = i & 63, kb = i >> 6;  // b tile: 16 k x 64 cols
+      const int64_t gc = col0 + cc;
+      bs[kb][cc] = (gc < M && k0 + kb < D) ? __ldg(b + (int64_t)(k0 + kb) * M + gc) : 0.0f;
+    }
+    __syncthreads();
+    const int kn = min(16, D - k0);
+    for (int kk = 0; kk < kn; ++kk) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float av = as[kk][ty * 4 + i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av, bs[kk][tx * 4 + j]));
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = row0 + ty * 4 + i;
+    if (r >= N) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t c = col0 + tx * 4 + j;
+      if (c < M) out[r * M + c] = acc[i][j];
+    }
+  }
+}
+
+int matmul_ref(const float* a, const float* b, int64_t n, int d, int m, float* out, cudaStream_t stream) {
+  if (n == 0 || m == 0) return LUT_OK;
+  const dim3 grid((unsigned)((m + 63) / 64), (unsigned)((n + 63) / 64));
+  if (grid.y > 65535u) return fail(LUT_ERR_CONFIG, "matmul_ref: too many rows for one launch");
+  matmul_ref_kernel<<<grid, 256, 0, stream>>>(a, b, (int)n, d, m, out);
+  LUT_CHECK_LAUNCH("matmul_ref_kernel");
+  return LUT_OK;
+}
+
 }  // namespace lutgpu

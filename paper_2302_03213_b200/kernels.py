@@ -9,6 +9,7 @@ host round trip.  There is no CPU fallback.
 
 from __future__ import annotations
 
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -342,3 +343,99 @@ def flop_counter(n: int, d: int, m: int, k: int, v: int) -> dict:
     if v < 1 or d % v != 0:
         raise ConfigError(f"D={d} not divisible by V={v}")
     return {"encode": n * d * k, "lookup_aggregate": n * m * (d // v), "dense": n * d * m}
+
+
+# ------------------------------------------------------------------- bench
+
+
+@dataclass
+class BenchReport:
+    """Timing of the LUT pipeline against the dense matmul_ref
+    (kernels.py:249-285).  Here both paths run on the GPU and are timed with
+    CUDA events on the launching stream (operands resident in HBM)."""
+
+    n: int
+    d: int
+    m: int
+    k: int
+    v: int
+    plan: KernelPlan
+    repetitions: int
+    lut_min_ns: int
+    lut_median_ns: int
+    dense_min_ns: int
+    dense_median_ns: int
+
+    @property
+    def gflops_equiv(self) -> float:
+        """Dense-equivalent MAC throughput of the LUT path, in G MAC/s."""
+        return (self.n * self.d * self.m) / self.lut_median_ns
+
+    @property
+    def speedup_vs_dense(self) -> float:
+        return self.dense_median_ns / self.lut_median_ns
+
+    CSV_HEADER = ("n,d,m,k,v,n_block,k_block,group_size,"
+                  "min_ns,median_ns,gflops_equiv,speedup_vs_dense")
+
+    def csv_row(self) -> str:
+        return (f"{self.n},{self.d},{self.m},{self.k},{self.v},"
+                f"{self.plan.n_block},{self.plan.k_block},{self.plan.group_size},"
+                f"{self.lut_min_ns},{self.lut_median_ns},"
+                f"{self.gflops_equiv:.6f},{self.speedup_vs_dense:.4f}")
+
+
+def _time_device(fn, repetitions: int, warmup: int) -> list[int]:
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    times = []
+    stream = torch.cuda.current_stream()
+    for _ in range(repetitions):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(int(e0.elapsed_time(e1) * 1e6))
+    return times
+
+
+def bench_kernel(shape, plan: KernelPlan = KernelPlan(), repetitions: int = 9, rng=None,
+                 warmup: int = 2) -> BenchReport:
+    """Time the quantized LUT pipeline (encode + int8 lookup-accumulate) and
+    the dense reference product on one (N, D, M, K, V) shape with random
+    operands (kernels.py:288-349); min and median over `repetitions`."""
+    n, d, m, k, v = shape
+    if repetitions < 5:
+        raise ConfigError(f"need at least 5 repetitions, got {repetitions}")
+    if d % v != 0:
+        raise ConfigError(f"D={d} not divisible by V={v}")
+    if rng is None:
+        rng = np.random.default_rng(0)
+    from .layer import LutLayer
+    from .pq import PqConfig
+
+    c_books = d // v
+    a = rng.standard_normal((n, d)).astype(F32)
+    books = rng.standard_normal((c_books, k, v)).astype(F32)
+    b = rng.standard_normal((d, m)).astype(F32)
+    dev = D.require_cuda()
+    a_dev, b_dev = D.to_device(a, F32, dev), D.to_device(b, F32, dev)
+    layer = LutLayer(cfg=PqConfig(v=v, k=k), books=books, weight=b_dev, qat=True, device=dev)
+    lib = load()
+    out = torch.empty((n, m), dtype=torch.float32, device=dev)
+    codes = torch.empty((n, layer.code_stride), dtype=torch.uint8, device=dev)
+
+    def lut_path():
+        layer.forward_device(a_dev, True, out=out, codes=codes)
+
+    def dense_path():
+        check(lib.lut_matmul_ref_f32(D.ptr(a_dev), D.ptr(b_dev), n, d, m, D.ptr(out), D.stream_ptr()),
+              "matmul_ref")
+
+    lut_t = _time_device(lut_path, repetitions, warmup)
+    dense_t = _time_device(dense_path, repetitions, warmup)
+    return BenchReport(n=n, d=d, m=m, k=k, v=v, plan=plan, repetitions=repetitions,
+                       lut_min_ns=int(np.min(lut_t)), lut_median_ns=int(np.median(lut_t)),
+                       dense_min_ns=int(np.min(dense_t)), dense_median_ns=int(np.median(dense_t)))

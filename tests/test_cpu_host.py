@@ -226,3 +226,24 @@ def test_bench_reference_arm_small():
     assert line["one_core"]["cores"] == 1 and "linear" in line["linearity"]
     assert line["config"]["rows_sampled_per_step"] == line["cpu_baseline"]["cores"] * 64
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_rng_and_split_dropins():
+    """make_rng / child_rng are the reference's Philox streams (rng.py:15-28);
+    split_subvectors returns D/v views (tensor.py:128-135)."""
+    import paper_2302_03213_b200 as L
+    from oracle import lut_oracle as O
+
+    assert np.array_equal(L.make_rng(42).integers(0, 2**63, 16), O.make_rng(42).integers(0, 2**63, 16))
+    assert np.array_equal(L.child_rng(7, 3).standard_normal(5), O.child_rng(7, 3).standard_normal(5))
+    assert not np.array_equal(L.child_rng(7, 0).standard_normal(5), L.make_rng(7).standard_normal(5))
+    with pytest.raises(ValueError):
+        L.child_rng(1, -1)
+    a = np.arange(24, dtype=F32).reshape(2, 12)
+    parts = L.split_subvectors(a, 4)
+    assert len(parts) == 3 and all(p.shape == (2, 4) for p in parts)
+    assert np.array_equal(np.concatenate(parts, axis=1), a)
+    with pytest.raises(L.ConfigError):
+        L.split_subvectors(a, 5)
+    with pytest.raises(L.ConfigError):
+        L.split_subvectors(a, 0)

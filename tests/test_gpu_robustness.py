@@ -183,3 +183,26 @@ def test_sharded_forward_two_ranks_bitwise(L):
         single = layer.forward_device(torch.from_numpy(a).cuda(), integer).cpu().numpy()
         for r in (0, 1):
             assert res[r][integer].tobytes() == single.tobytes(), (r, integer)
+
+
+@pytest.mark.parametrize("n,d,m", [(1, 1, 1), (70, 33, 65), (300, 256, 130), (64, 0, 8)])
+def test_matmul_ref_bitwise(L, n, d, m):
+    """The dense baseline (tensor.py:110-125) on the GPU: bitwise equal to the
+    ascending-k f32 loop."""
+    rng = O.make_rng(n + d + m)
+    a = rng.standard_normal((n, d)).astype(F32)
+    b = rng.standard_normal((d, m)).astype(F32)
+    got = L.matmul_ref(a, b)
+    assert got.dtype == np.float32 and got.tobytes() == O.matmul_ref(a, b).tobytes()
+
+
+def test_bench_kernel_report(L):
+    """bench_kernel / BenchReport (kernels.py:249-349): GPU-timed LUT path vs
+    the dense matmul_ref, CSV row in the reference's column order."""
+    rep = L.bench_kernel((512, 256, 128, 16, 16), repetitions=5)
+    assert rep.lut_min_ns > 0 and rep.dense_median_ns > 0 and rep.gflops_equiv > 0
+    assert rep.csv_row().count(",") == L.BenchReport.CSV_HEADER.count(",")
+    with pytest.raises(L.ConfigError):
+        L.bench_kernel((8, 10, 4, 4, 3))
+    with pytest.raises(L.ConfigError):
+        L.bench_kernel((8, 8, 4, 4, 2), repetitions=3)
