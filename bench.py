@@ -52,7 +52,10 @@ def parse():
     p.add_argument("--cpu-rows", type=int, default=0, help="CPU sample rows per core (0 = default)")
     p.add_argument("--workload", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"], default="cfg5",
                    help="BASELINE configs[i-1]; cfg5 (default) is the headline scaling sweep")
-    p.add_argument("--scale-mtile", type=int, default=0, help="cfg2/cfg4: per-m-tile int8 scales (0 = per table)")
+    p.add_argument("--scale-mtile", type=int, default=-1,
+                   help="cfg2/cfg4: per-m-tile int8 scales (0 = per table; default: cfg2 128, cfg4 0)")
+    p.add_argument("--per-table-scales", action="store_true",
+                   help="cfg2: one scale per (m-tile) shared by all codebooks instead of BASELINE's per-(c, m-tile)")
     p.add_argument("--no-variants", action="store_true", help="skip the K=64 / fp32 / CUDA-core variant timings")
     p.add_argument("--no-ties", action="store_true", help="skip the f64 near-tie count")
     p.add_argument("--gather-out", action="store_true",
@@ -566,7 +569,9 @@ def main_stack(args):
         mod = LutLinear(layer, integer)
         fn, rows, unit_rows = (lambda: mod(x)), 1024, "rows"
     elif wl == "cfg2":
-        ffn, x = W.ffn_pair(dev, tokens=4096, scale_mtile=args.scale_mtile)
+        # BASELINE configs[1]: int8 tables with a per-(c, m-tile) fp32 scale
+        mt = 128 if args.scale_mtile < 0 else args.scale_mtile
+        ffn, x = W.ffn_pair(dev, tokens=4096, scale_mtile=mt, per_codebook=not args.per_table_scales)
         fn, rows, unit_rows = (lambda: ffn(x)), 4096, "tokens"
     elif wl == "cfg3":
         convs = W.resnet_convs(dev, batch=256)
@@ -579,7 +584,7 @@ def main_stack(args):
         rows = sum(xx.shape[0] * xx.shape[2] * xx.shape[3] for _, xx in convs)
         unit_rows = "output pixels"
     else:
-        model, x = W.bert_encoder(dev, batch=64, seq=128, scale_mtile=args.scale_mtile)
+        model, x = W.bert_encoder(dev, batch=64, seq=128, scale_mtile=max(0, args.scale_mtile))
         fn, rows, unit_rows = (lambda: model(x)), 64 * 128, "tokens"
 
     # per-LUT-layer events + algorithmic HBM bytes (fused layer formula)
@@ -636,7 +641,11 @@ def main_stack(args):
         graph = None
         print(f"graph capture failed: {exc!r}", file=sys.stderr)
     run = graph.replay if graph is not None else fn
+    # L2 flush between timed steps: write a 256 MB buffer (> 126 MB L2), then read
+    # a second one so the write-back of the flush's dirty lines happens here and
+    # not inside the next timed step (L2 is left holding clean, unrelated lines)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_rd = torch.ones(64 << 20, dtype=torch.float32, device=dev)
     for _ in range(args.warmup):
         run()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -646,6 +655,7 @@ def main_stack(args):
     with ClockSampler(local) as clocks:
         for e0, e1 in evs:
             flush.zero_()
+            flush_rd.sum()
             e0.record()
             run()
             e1.record()
@@ -687,7 +697,10 @@ def main_stack(args):
             "data": "synthetic (seeded torch.randn on device; random-init weights; centroids sampled from a "
                     "held-out batch)",
             "config": {"workload": STACKS[wl], "rows_per_step": rows, "cuda_graph": graph is not None,
-                       "l2": "256 MB buffer written between timed steps", "scale_mtile": args.scale_mtile},
+                       "l2": "256 MB buffer written, then a 256 MB buffer read, between timed steps",
+                       "scale_mtile": args.scale_mtile,
+                       **({"int8_scales": "per (m-tile)" if args.per_table_scales else "per (codebook, m-tile)"}
+                          if wl == "cfg2" else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": None, "kernel": "LUT layers (encode+gather)",
                          "peak_kind": peak_kind, "algorithmic_bytes": lut_bytes, "lut_ms_eager": lut_ms,

@@ -15,8 +15,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "liblutgpu.so")
-SOURCES = ["capi.cu", "encode.cu", "encode_tc.cu", "gather.cu", "onehot.cu", "table.cu"]
-HEADERS = ["common.cuh"]
+SOURCES = ["capi.cu", "encode.cu", "encode_tc.cu", "gather.cu", "onehot.cu", "onehot_stream.cu", "table.cu"]
+HEADERS = ["common.cuh", "onehot_dev.cuh"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

@@ -275,7 +275,7 @@ def _lut_record(lut, conv, quantize_table) -> LutRecord:
     if getattr(lut, "qat", False) or qt is not None:
         if qt is None or has_bias:
             qt = quantize_table(table)
-        if getattr(qt, "scale_mtile", 0):
+        if getattr(qt, "scale_mtile", 0) or getattr(qt, "per_codebook", False):
             raise ContainerError("per-m-tile int8 scales cannot be stored in a version-1 container")
         rec.q = _host(qt.q, np.int8)
         rec.scale = float(_host(qt.scale, F32).reshape(-1)[0])

@@ -7,7 +7,10 @@
 
 #include <nvtx3/nvToolsExt.h>
 
+#include <map>
 #include <mutex>
+#include <tuple>
+#include <utility>
 #include <string>
 
 #include "common.cuh"
@@ -79,16 +82,67 @@ int cuda_fail(cudaError_t e, const char* where) {
   return LUT_ERR_CUDA;
 }
 
+static int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  return dev;
+}
+
 int num_sms() {
-  int dev = 0, n = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n > 0 ? n : 148;
+  static int cache[64] = {};
+  const int dev = current_device();
+  if (!cache[dev]) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
 }
 
 size_t max_smem_optin() {
-  int dev = 0, n = 227 * 1024;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  return (size_t)n;
+  static int cache[64] = {};
+  const int dev = current_device();
+  if (!cache[dev]) {
+    int n = 227 * 1024;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cache[dev] = n;
+  }
+  return (size_t)cache[dev];
+}
+
+// Per-(kernel, device) launch setup, done once: the dynamic shared-memory limit
+// is raised to the device maximum, and occupancies are cached per (threads,
+// smem).  Both driver calls cost microseconds, which small LUT layers (tens of
+// microseconds of GPU time) would otherwise pay on every call.
+namespace {
+std::mutex g_kernel_mu;
+std::map<std::pair<const void*, int>, bool> g_smem_set;
+std::map<std::tuple<const void*, int, int, size_t>, int> g_occ;
+}  // namespace
+
+cudaError_t kernel_smem_attr(const void* func) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_kernel_mu);
+  auto key = std::make_pair(func, dev);
+  if (g_smem_set.count(key)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem_optin());
+  if (e == cudaSuccess) g_smem_set[key] = true;
+  return e;
+}
+
+int kernel_occupancy(const void* func, int threads, size_t smem) {
+  const int dev = current_device();
+  {
+    std::lock_guard<std::mutex> lk(g_kernel_mu);
+    auto it = g_occ.find(std::make_tuple(func, dev, threads, smem));
+    if (it != g_occ.end()) return it->second;
+  }
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, threads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  std::lock_guard<std::mutex> lk(g_kernel_mu);
+  g_occ[std::make_tuple(func, dev, threads, smem)] = per_sm;
+  return per_sm;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

@@ -20,6 +20,10 @@ int fail(int status, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);
 int num_sms();
 size_t max_smem_optin();
+// once per (kernel, device): dynamic SMEM limit raised to the device maximum
+cudaError_t kernel_smem_attr(const void* func);
+// cached cudaOccupancyMaxActiveBlocksPerMultiprocessor
+int kernel_occupancy(const void* func, int threads, size_t smem);
 
 // Tuning / ablation knobs (LUTGPU_OH_*, LUTGPU_ENC_*, ...) are read only in
 // probe builds (-DLUTGPU_PROBES, tools/build_probes.sh); the product build never

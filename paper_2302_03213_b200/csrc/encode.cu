@@ -699,7 +699,7 @@ static int launch_conv_plane(const float* x, int batch, int cin, int h, int w, i
   p.code_stride = code_stride;
   p.near_tie = near_tie;
   auto kern = encode_conv_plane_kernel<K, KH>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = kernel_smem_attr(reinterpret_cast<const void*>(kern));
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(encode_conv_plane)");
   const int nsm = num_sms();
   const int grid = (int)(p.nunits < nsm ? p.nunits : nsm);
@@ -767,11 +767,11 @@ static int launch_rows(const DenseRows* dense, const ConvRows* conv, int64_t n, 
   do {                                                                                                 \
     if (dense) {                                                                                       \
       auto kern = encode_rows_kernel<VT, DenseRows>;                                                   \
-      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (smem > 48 * 1024) kernel_smem_attr(reinterpret_cast<const void*>(kern)); \
       kern<<<grid, 256, smem, stream>>>(*dense, n, prep, S, C, K, V, codes, code_bits, code_stride, near_tie); \
     } else {                                                                                           \
       auto kern = encode_rows_kernel<VT, ConvRows>;                                                    \
-      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (smem > 48 * 1024) kernel_smem_attr(reinterpret_cast<const void*>(kern)); \
       kern<<<grid, 256, smem, stream>>>(*conv, n, prep, S, C, K, V, codes, code_bits, code_stride, near_tie); \
     }                                                                                                  \
   } while (0)
@@ -842,7 +842,7 @@ static int launch_tma(const float* a, int64_t n, int d, const float* prep, int C
   auto kern = rpl == 2 ? (chain ? encode_tma_kernel<V, 8, 2, 1> : encode_tma_kernel<V, 8, 2, 0>)
                        : (chain ? encode_tma_kernel<V, 4, 4, 1> : encode_tma_kernel<V, 4, 4, 0>);
   const int threads = rpl == 2 ? 9 * 32 : 5 * 32;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = kernel_smem_attr(reinterpret_cast<const void*>(kern));
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(encode_tma)");
   kern<<<grid, threads, smem, stream>>>(tmap, p);
   LUT_CHECK_LAUNCH("encode_tma_kernel");

@@ -421,7 +421,7 @@ int encode_dense_tc(const float* a, int64_t n, int d, const float* prep, int C, 
   const size_t sb = K == 16 ? tc_stage_bytes<16>() : tc_stage_bytes<64>();
   const size_t smem = (((size_t)stages * sb + 3 * stages * sizeof(uint64_t) + 16 + 127) & ~size_t(127)) + 4096 + 1024;
   if (smem > max_smem_optin()) return LUT_OK;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = kernel_smem_attr(reinterpret_cast<const void*>(kern));
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(encode_tc)");
   kern<<<grid, (2 + 4 * gr) * 32, smem, stream>>>(tmap, p);
   LUT_CHECK_LAUNCH("encode_tc_kernel");

@@ -7,9 +7,10 @@
 //         out = act(fl(fl(f32(acc) * scale) + bias)) — bitwise equal to
 //         lut_gather_i32 + lut_gather_accumulate (kernels.py:105-135).
 //
-// Tiled kernels are table-stationary: a persistent CTA owns an m-tile, stages
-// the (C, K, MT) table slice in shared memory once, and streams rows through
-// it.  fp32: each lane owns 4 consecutive outputs (LDS.128 per lookup).
+// The tiled kernels are table-stationary and row-parallel (thread = row): a CTA
+// owns an m-tile, stages its (C, K, MT) table slice in shared memory in a
+// chunk-major layout that lets the LSU broadcast repeated lookups, and streams
+// row blocks through it.  fp32 sums with packed add.rn.f32x2 (two IEEE adds).
 // int8: the slice is stored biased (q + 128, 1..255) so four int8 lookups
 // are summed with two 32-bit adds into u16 pairs (<= 256 codebooks per pair
 // group: 256 * 255 < 65536), widened to int32 after every 256 codebooks —
@@ -122,238 +123,403 @@ __global__ void gather_i8_generic(GatherArgs g, const int8_t* __restrict__ q) {
   }
 }
 
-// ------------------------------------------------------------ tiled f32
+// ------------------------------------------------------------ row-parallel tiled
+//
+// Thread = one row.  A CTA owns an m-tile (MT output columns) and stages the
+// table slice for it in SMEM as [c][chunk][k][8 B] (f32: a chunk = 2 columns;
+// int8: 8 columns).  For a given (c, chunk) a half-warp's 16 lanes read at most
+// K distinct 8-byte chunks of one K*8-byte region: for K <= 16 that region is
+// one 128-byte bank row, so every LDS.64 is conflict-free (equal codes are
+// broadcast) and a warp's lookup costs exactly 2 wavefronts — the SMEM
+// roofline of 128 B/clk/SM, where the column-parallel layout [c][k][m] loses
+// ~40% to bank conflicts between rows.
+// Units = (m-tile, row block), walked in row bands so the band's codes stay
+// in L2 while every CTA re-stages its slice only when its m-tile changes.
 
-constexpr int kGatherThreads = 256;
-
-template <int MT>
-__global__ void __launch_bounds__(kGatherThreads)
-    gather_f32_tiled(GatherArgs g, const float* __restrict__ table) {
-  constexpr int LPR = MT / 4;             // lanes per row
-  constexpr int RPW = 32 / LPR;           // rows per warp
-  constexpr int RPT = 4;                  // rows per thread per pass
-  constexpr int ROWS = RPW * (kGatherThreads / 32) * RPT;
-  extern __shared__ float4 tsm4[];
-  float* tsm = reinterpret_cast<float*>(tsm4);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q = lane % LPR, rsub = lane / LPR;
-  const int nmt = (g.M + MT - 1) / MT;
-  const int64_t nrb = (g.n + ROWS - 1) / ROWS;
-  const int cpm = gridDim.x >= (unsigned)nmt ? gridDim.x / nmt : 1;  // CTAs per m-tile
-  const int first_mt = blockIdx.x % nmt;
-  const int split = gridDim.x >= (unsigned)nmt ? blockIdx.x / nmt : 0;
-  if (split >= cpm) return;
-  const int64_t rb_per = (nrb + cpm - 1) / cpm;
-  const int64_t rb0 = split * rb_per, rb1 = min(nrb, rb0 + rb_per);
-  const int mt_step = gridDim.x >= (unsigned)nmt ? nmt : gridDim.x;
-  const bool words = g.code_bits == 8 ? ((g.code_stride & 3) == 0 && (reinterpret_cast<uintptr_t>(g.codes) & 3) == 0)
-                                      : ((g.code_stride & 3) == 0 && (reinterpret_cast<uintptr_t>(g.codes) & 3) == 0);
-  const int span = g.code_bits == 8 ? 4 : 8;
-
-  for (int mt = first_mt; mt < nmt; mt += mt_step) {
-    const int m0 = mt * MT;
-    __syncthreads();
-    const bool vec = (g.M & 3) == 0 && (reinterpret_cast<uintptr_t>(table) & 15) == 0;
-    for (int i = threadIdx.x; i < g.C * g.K * LPR; i += blockDim.x) {
-      const int ck = i / LPR, qq = i - ck * LPR;
-      const int col = m0 + 4 * qq;
-      const float* src = table + (int64_t)ck * g.M + col;
-      float4 v;
-      if (vec && col + 3 < g.M) {
-        v = __ldg(reinterpret_cast<const float4*>(src));  // one 16-byte load per 4 columns
-      } else {
-        v.x = col + 0 < g.M ? __ldg(src + 0) : 0.0f;
-        v.y = col + 1 < g.M ? __ldg(src + 1) : 0.0f;
-        v.z = col + 2 < g.M ? __ldg(src + 2) : 0.0f;
-        v.w = col + 3 < g.M ? __ldg(src + 3) : 0.0f;
-      }
-      tsm4[i] = v;
+struct RowWalk {
+  int64_t nrb, band_rb, band, nbands, left, rbl, brb;
+  int nmt, mt, slot, nslots;
+  __device__ void init(int64_t nrb_, int nmt_, int64_t band_rb_) {
+    nrb = nrb_;
+    nmt = nmt_;
+    band_rb = band_rb_;
+    slot = (int)blockIdx.x;
+    nslots = (int)gridDim.x;
+    nbands = (nrb + band_rb - 1) / band_rb;
+    band = -1;
+    left = 0;
+  }
+  __device__ bool next(int& mt_out, int64_t& rb_out) {
+    while (left == 0) {
+      if (++band >= nbands) return false;
+      brb = min(band_rb, nrb - band * band_rb);
+      const int64_t ub = (int64_t)nmt * brb;
+      const int64_t lo = ub * slot / nslots, hi = ub * (slot + 1) / nslots;
+      left = hi - lo;
+      mt = (int)(lo / brb);
+      rbl = lo - (int64_t)mt * brb;
     }
-    __syncthreads();
-    const int col0 = m0 + 4 * q;
-    for (int64_t rb = rb0; rb < rb1; ++rb) {
-      int64_t rows[RPT];
-      float4 acc[RPT];
+    mt_out = mt;
+    rb_out = band * band_rb + rbl;
+    --left;
+    if (++rbl == brb) {
+      rbl = 0;
+      ++mt;
+    }
+    return true;
+  }
+};
+
+// Codes of one row, 16 at a time when the rows are 16-byte aligned.
+struct RowCodes {
+  const uint8_t* p;
+  bool v16;
+  __device__ __forceinline__ uint4 load16(int c0) const {
+    if (v16) return __ldg(reinterpret_cast<const uint4*>(p + c0));
+    uint32_t w[4];
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        rows[r] = rb * ROWS + (int64_t)r * (RPW * (kGatherThreads / 32)) + warp * RPW + rsub;
-        acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      int c = 0;
-      if (words) {
-        const int cfull = (g.C / span) * span;
-        for (; c < cfull; c += span) {
-          uint32_t w[RPT];
+    for (int i = 0; i < 4; ++i)
+      w[i] = (uint32_t)__ldg(p + c0 + 4 * i) | ((uint32_t)__ldg(p + c0 + 4 * i + 1) << 8) |
+             ((uint32_t)__ldg(p + c0 + 4 * i + 2) << 16) | ((uint32_t)__ldg(p + c0 + 4 * i + 3) << 24);
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+
+__device__ __forceinline__ uint32_t code_byte(const uint4& w, int s) {
+  const uint32_t x = s < 4 ? w.x : s < 8 ? w.y : s < 12 ? w.z : w.w;
+  return (x >> (8 * (s & 3))) & 255u;
+}
+
+// Range check of 16 codes (any code >= K raises CorruptionError through the
+// error flag; the lookup then reads a clamped entry, the result is discarded).
+__device__ __forceinline__ bool codes_bad(const uint4& w, int K, int pow2) {
+  if (pow2) {
+    const uint32_t hi = 0x01010101u * (uint32_t)(0xFF & ~(K - 1));
+    return ((w.x | w.y | w.z | w.w) & hi) != 0u;
+  }
+  bool bad = false;
 #pragma unroll
-          for (int r = 0; r < RPT; ++r) {
-            const int64_t rr = rows[r] < g.n ? rows[r] : g.n - 1;
-            w[r] = __ldg(reinterpret_cast<const uint32_t*>(g.codes + rr * g.code_stride +
-                                                          (g.code_bits == 8 ? c : (c >> 1))));
-          }
-          for (int s = 0; s < span; ++s) {
+  for (int s = 0; s < 16; ++s) bad |= code_byte(w, s) >= (uint32_t)K;
+  return bad;
+}
+
+__device__ __forceinline__ uint64_t lds64(uint32_t saddr) {
+  uint64_t v;
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(saddr));
+  return v;
+}
+
+__device__ __forceinline__ void fadd2(uint64_t& a, uint64_t t) {
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(a) : "l"(t));  // two IEEE fp32 adds
+}
+
+// Stage the m-tile's table slice: 8 loads in flight per thread (the slice is
+// read once per m-tile change; a load-then-store loop is latency-bound on a
+// cold L2).  f32 chunk = 2 columns, the (c, k) row segment read as float2.
+template <int NP, int T>
+__device__ __forceinline__ void stage_f32_slice(uint2* tsm, const float* __restrict__ table, int M, int C, int K,
+                                                int m0) {
+  const int total = C * K * NP;
+  const bool vec = (M & 1) == 0 && (reinterpret_cast<uintptr_t>(table) & 7) == 0;
+  const int lk = (K & (K - 1)) == 0 ? __ffs(K) - 1 : -1;
+  for (int base = threadIdx.x; base < total; base += 8 * T) {
+    uint2 v[8];
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) {
-              int code = g.code_bits == 8 ? (int)((w[r] >> (8 * s)) & 255u) : (int)((w[r] >> (4 * s)) & 15u);
-              code = checked(g, code);
-              const float4 t = tsm4[((c + s) * g.K + code) * LPR + q];
-              acc[r].x = __fadd_rn(acc[r].x, t.x);
-              acc[r].y = __fadd_rn(acc[r].y, t.y);
-              acc[r].z = __fadd_rn(acc[r].z, t.z);
-              acc[r].w = __fadd_rn(acc[r].w, t.w);
-            }
-          }
-        }
-      }
-      for (; c < g.C; ++c) {
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          const int64_t rr = rows[r] < g.n ? rows[r] : g.n - 1;
-          const int code = checked(g, read_code(g, rr, c));
-          const float4 t = tsm4[(c * g.K + code) * LPR + q];
-          acc[r].x = __fadd_rn(acc[r].x, t.x);
-          acc[r].y = __fadd_rn(acc[r].y, t.y);
-          acc[r].z = __fadd_rn(acc[r].z, t.z);
-          acc[r].w = __fadd_rn(acc[r].w, t.w);
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        if (rows[r] >= g.n) continue;
-        float v[4] = {acc[r].x, acc[r].y, acc[r].z, acc[r].w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) v[e] = (col0 + e < g.M) ? f32_epilogue(g, v[e], col0 + e) : 0.f;
-        if (g.out_hw == 0 && col0 + 3 < g.M && (g.M & 3) == 0 &&
-            (reinterpret_cast<uintptr_t>(g.out) & 15) == 0) {
-          *reinterpret_cast<float4*>(g.out + rows[r] * g.M + col0) = make_float4(v[0], v[1], v[2], v[3]);
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * T;
+      if (i < total) {
+        const int ck = i / NP, j = i - ck * NP;
+        const int col = m0 + 2 * j;
+        const float* src = table + (int64_t)ck * M + col;
+        if (vec && col + 1 < M) {
+          v[u] = __ldg(reinterpret_cast<const uint2*>(src));
         } else {
-          int64_t base, cs;
-          out_row(g, rows[r], base, cs);
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (col0 + e < g.M) g.out[base + (int64_t)(col0 + e) * cs] = v[e];
+          v[u].x = col < M ? __float_as_uint(__ldg(src)) : 0u;
+          v[u].y = col + 1 < M ? __float_as_uint(__ldg(src + 1)) : 0u;
         }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * T;
+      if (i < total) {
+        const int ck = i / NP, j = i - ck * NP;
+        const int c = lk >= 0 ? ck >> lk : ck / K, k = ck - c * K;
+        tsm[(c * NP + j) * K + k] = v[u];
       }
     }
   }
 }
 
-// ------------------------------------------------------------ tiled int8
-
-template <int MT>
-__global__ void __launch_bounds__(kGatherThreads)
-    gather_i8_tiled(GatherArgs g, const int8_t* __restrict__ q8) {
-  constexpr int LPR = MT / 16;            // lanes per row, 16 columns each
-  constexpr int RPW = 32 / LPR;
-  constexpr int RPT = 2;
-  constexpr int ROWS = RPW * (kGatherThreads / 32) * RPT;
-  extern __shared__ uint4 qsm4[];
-  uint8_t* qsm = reinterpret_cast<uint8_t*>(qsm4);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ql = lane % LPR, rsub = lane / LPR;
-  const int nmt = (g.M + MT - 1) / MT;
-  const int64_t nrb = (g.n + ROWS - 1) / ROWS;
-  const int cpm = gridDim.x >= (unsigned)nmt ? gridDim.x / nmt : 1;
-  const int first_mt = blockIdx.x % nmt;
-  const int split = gridDim.x >= (unsigned)nmt ? blockIdx.x / nmt : 0;
-  if (split >= cpm) return;
-  const int64_t rb_per = (nrb + cpm - 1) / cpm;
-  const int64_t rb0 = split * rb_per, rb1 = min(nrb, rb0 + rb_per);
-  const int mt_step = gridDim.x >= (unsigned)nmt ? nmt : gridDim.x;
-  const bool words = (g.code_stride & 3) == 0 && (reinterpret_cast<uintptr_t>(g.codes) & 3) == 0;
-  const int span = g.code_bits == 8 ? 4 : 8;
-  uint32_t cw[RPT];
-  int have = 0;
-
-  for (int mt = first_mt; mt < nmt; mt += mt_step) {
-    const int m0 = mt * MT;
-    __syncthreads();
-    for (int i = threadIdx.x; i < g.C * g.K * MT; i += blockDim.x) {
-      const int ck = i / MT, cc = i - ck * MT;
-      const int col = m0 + cc;
-      const int v = col < g.M ? (int)__ldg(q8 + (int64_t)ck * g.M + col) : 0;
-      qsm[i] = (uint8_t)(v + 128);
-    }
-    __syncthreads();
-    const int col0 = m0 + 16 * ql;
-    for (int64_t rb = rb0; rb < rb1; ++rb) {
-      int64_t rows[RPT];
-      int tot[RPT][16];
+// int8 chunk = 8 columns, stored biased (q + 128 = q ^ 0x80 per byte).
+template <int NO, int T>
+__device__ __forceinline__ void stage_i8_slice(uint2* qsm, const int8_t* __restrict__ q8, int M, int C, int K,
+                                               int m0) {
+  const int total = C * K * NO;
+  const bool vec = (M & 7) == 0 && (reinterpret_cast<uintptr_t>(q8) & 7) == 0;
+  const int lk = (K & (K - 1)) == 0 ? __ffs(K) - 1 : -1;
+  for (int base = threadIdx.x; base < total; base += 8 * T) {
+    uint2 v[8];
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        rows[r] = rb * ROWS + (int64_t)r * (RPW * (kGatherThreads / 32)) + warp * RPW + rsub;
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * T;
+      if (i < total) {
+        const int ck = i / NO, j = i - ck * NO;
+        const int col = m0 + 8 * j;
+        const int8_t* src = q8 + (int64_t)ck * M + col;
+        if (vec && col + 7 < M) {
+          v[u] = __ldg(reinterpret_cast<const uint2*>(src));
+        } else {
+          uint32_t w[2] = {0u, 0u};
 #pragma unroll
-        for (int e = 0; e < 16; ++e) tot[r][e] = 0;
-      }
-      for (int c0 = 0; c0 < g.C; c0 += 256) {
-        const int c1 = min(g.C, c0 + 256);
-        uint32_t lo[RPT][4], hi[RPT][4];
-#pragma unroll
-        for (int r = 0; r < RPT; ++r)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) lo[r][i] = hi[r][i] = 0u;
-        for (int c = c0; c < c1; ++c) {
-          if (words && (c & (span - 1)) == 0 && c + span <= c1) {
-#pragma unroll
-            for (int r = 0; r < RPT; ++r) {
-              const int64_t rr = rows[r] < g.n ? rows[r] : g.n - 1;
-              cw[r] = __ldg(reinterpret_cast<const uint32_t*>(g.codes + rr * g.code_stride +
-                                                             (g.code_bits == 8 ? c : (c >> 1))));
-            }
-            have = span;
-          }
-#pragma unroll
-          for (int r = 0; r < RPT; ++r) {
-            int code;
-            if (have > 0) {
-              code = g.code_bits == 8 ? (int)(cw[r] & 255u) : (int)(cw[r] & 15u);
-              cw[r] = g.code_bits == 8 ? (cw[r] >> 8) : (cw[r] >> 4);
-            } else {
-              const int64_t rr = rows[r] < g.n ? rows[r] : g.n - 1;
-              code = read_code(g, rr, c);
-            }
-            code = checked(g, code);
-            const uint4 t = qsm4[((c * g.K + code) * MT >> 4) + ql];
-            lo[r][0] += t.x & 0x00FF00FFu;
-            hi[r][0] += (t.x >> 8) & 0x00FF00FFu;
-            lo[r][1] += t.y & 0x00FF00FFu;
-            hi[r][1] += (t.y >> 8) & 0x00FF00FFu;
-            lo[r][2] += t.z & 0x00FF00FFu;
-            hi[r][2] += (t.z >> 8) & 0x00FF00FFu;
-            lo[r][3] += t.w & 0x00FF00FFu;
-            hi[r][3] += (t.w >> 8) & 0x00FF00FFu;
-          }
-          if (have > 0) --have;
+          for (int e = 0; e < 8; ++e)
+            if (col + e < M) w[e >> 2] |= (uint32_t)(uint8_t)__ldg(src + e) << (8 * (e & 3));
+          v[u] = make_uint2(w[0], w[1]);
         }
-        const int bias128 = 128 * (c1 - c0);
+      }
+    }
 #pragma unroll
-        for (int r = 0; r < RPT; ++r)
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * T;
+      if (i < total) {
+        const int ck = i / NO, j = i - ck * NO;
+        const int c = lk >= 0 ? ck >> lk : ck / K, k = ck - c * K;
+        // columns beyond M stay 0 + 128 (their sums are never stored)
+        qsm[(c * NO + j) * K + k] = make_uint2(v[u].x ^ 0x80808080u, v[u].y ^ 0x80808080u);
+      }
+    }
+  }
+}
+
+// Thread block of T threads; NP chunks of 2 f32 columns per thread (MT = 2 * NP).
+template <int NP, int T>
+__global__ void __launch_bounds__(T, 1)
+    gather_f32_rows(GatherArgs g, const float* __restrict__ table, int64_t band_rb) {
+  extern __shared__ uint2 tsm[];  // [C][NP][K] float pairs
+  constexpr int MT = 2 * NP;
+  const int nmt = (g.M + MT - 1) / MT;
+  const int64_t nrb = (g.n + T - 1) / T;
+  const int K = g.K, C = g.C;
+  const int pow2 = (K & (K - 1)) == 0;
+  const bool v16 = g.code_bits == 8 && (g.code_stride & 15) == 0 && (reinterpret_cast<uintptr_t>(g.codes) & 15) == 0;
+  const uint32_t sbase = smem_u32(tsm);
+  const uint32_t cstep = (uint32_t)(NP * K * 8);  // bytes per codebook
+  RowWalk walk;
+  walk.init(nrb, nmt, band_rb);
+  int cur = -1;
+  int mt;
+  int64_t rb;
+  bool bad = false;
+  while (walk.next(mt, rb)) {
+    const int m0 = mt * MT;
+    if (mt != cur) {
+      __syncthreads();
+      stage_f32_slice<NP, T>(tsm, table, g.M, C, K, m0);
+      __syncthreads();
+      cur = mt;
+    }
+    const int64_t row = rb * T + threadIdx.x;
+    const bool live = row < g.n;
+    const int64_t rr = live ? row : g.n - 1;
+    uint64_t acc[NP];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            tot[r][4 * i + 0] += (int)(lo[r][i] & 0xFFFFu) - bias128;
-            tot[r][4 * i + 2] += (int)(lo[r][i] >> 16) - bias128;
-            tot[r][4 * i + 1] += (int)(hi[r][i] & 0xFFFFu) - bias128;
-            tot[r][4 * i + 3] += (int)(hi[r][i] >> 16) - bias128;
+    for (int j = 0; j < NP; ++j) acc[j] = 0ull;  // (+0.0f, +0.0f)
+    if (g.code_bits == 8) {
+      RowCodes rc{g.codes + rr * g.code_stride, v16};
+      int c0 = 0;
+      for (; c0 + 16 <= C; c0 += 16) {
+        const uint4 w = rc.load16(c0);
+        bad |= codes_bad(w, K, pow2);
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+          uint32_t code = code_byte(w, s);
+          code = pow2 ? (code & (uint32_t)(K - 1)) : min(code, (uint32_t)(K - 1));
+          const uint32_t a = sbase + (uint32_t)(c0 + s) * cstep + code * 8u;
+#pragma unroll
+          for (int j = 0; j < NP; ++j) fadd2(acc[j], lds64(a + (uint32_t)(j * K * 8)));
+        }
+      }
+      for (; c0 < C; ++c0) {
+        uint32_t code = __ldg(rc.p + c0);
+        bad |= code >= (uint32_t)K;
+        code = min(code, (uint32_t)(K - 1));
+        const uint32_t a = sbase + (uint32_t)c0 * cstep + code * 8u;
+#pragma unroll
+        for (int j = 0; j < NP; ++j) fadd2(acc[j], lds64(a + (uint32_t)(j * K * 8)));
+      }
+    } else {
+      for (int c = 0; c < C; ++c) {
+        uint32_t code = (uint32_t)read_code(g, rr, c);
+        bad |= code >= (uint32_t)K;
+        code = min(code, (uint32_t)(K - 1));
+        const uint32_t a = sbase + (uint32_t)c * cstep + code * 8u;
+#pragma unroll
+        for (int j = 0; j < NP; ++j) fadd2(acc[j], lds64(a + (uint32_t)(j * K * 8)));
+      }
+    }
+    if (!live) continue;
+    int64_t obase, ocs;
+    out_row(g, row, obase, ocs);
+    const bool vrow = ocs == 1 && (g.M & 3) == 0 && (reinterpret_cast<uintptr_t>(g.out) & 15) == 0;
+#pragma unroll
+    for (int j = 0; j < NP; j += 2) {
+      float v[4];
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(v[0]), "=f"(v[1]) : "l"(acc[j]));
+      if (j + 1 < NP) {
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(v[2]), "=f"(v[3]) : "l"(acc[j + 1]));
+      } else {
+        v[2] = v[3] = 0.f;
+      }
+      const int col = m0 + 2 * j;
+      const int ncol = j + 1 < NP ? 4 : 2;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = (e < ncol && col + e < g.M) ? f32_epilogue(g, v[e], col + e) : 0.f;
+      if (vrow && ncol == 4 && col + 3 < g.M) {
+        *reinterpret_cast<float4*>(g.out + obase + col) = make_float4(v[0], v[1], v[2], v[3]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (e < ncol && col + e < g.M) g.out[obase + (int64_t)(col + e) * ocs] = v[e];
+      }
+    }
+  }
+  if (bad && g.err) atomicMax(g.err, (int)LUT_ERR_CORRUPTION);
+}
+
+template <int NO>
+__device__ __forceinline__ void i8_lookup(uint32_t (&acc)[NO][4], uint32_t cbase, uint32_t code, int K) {
+  const uint32_t a = cbase + code * 8u;
+#pragma unroll
+  for (int j = 0; j < NO; ++j) {
+    const uint64_t t = lds64(a + (uint32_t)(j * K * 8));
+    const uint32_t w0 = (uint32_t)t, w1 = (uint32_t)(t >> 32);
+    acc[j][0] += __byte_perm(w0, 0, 0x4240);  // biased bytes 0, 2 -> u16 lanes
+    acc[j][1] += __byte_perm(w0, 0, 0x4341);  // bytes 1, 3
+    acc[j][2] += __byte_perm(w1, 0, 0x4240);
+    acc[j][3] += __byte_perm(w1, 0, 0x4341);
+  }
+}
+
+// int8: NO chunks of 8 columns per thread (MT = 8 * NO); biased bytes (q + 128)
+// summed as u16 pairs, widened every 256 codebooks when WIDE.
+template <int NO, bool WIDE, int T>
+__global__ void __launch_bounds__(T, 1)
+    gather_i8_rows(GatherArgs g, const int8_t* __restrict__ q8, int64_t band_rb) {
+  extern __shared__ uint2 qsm[];  // [C][NO][K] x 8 biased bytes
+  constexpr int MT = 8 * NO;
+  const int nmt = (g.M + MT - 1) / MT;
+  const int64_t nrb = (g.n + T - 1) / T;
+  const int K = g.K, C = g.C;
+  const int pow2 = (K & (K - 1)) == 0;
+  const bool v16 = g.code_bits == 8 && (g.code_stride & 15) == 0 && (reinterpret_cast<uintptr_t>(g.codes) & 15) == 0;
+  const uint32_t sbase = smem_u32(qsm);
+  const uint32_t cstep = (uint32_t)(NO * K * 8);
+  RowWalk walk;
+  walk.init(nrb, nmt, band_rb);
+  int cur = -1;
+  int mt;
+  int64_t rb;
+  bool bad = false;
+  while (walk.next(mt, rb)) {
+    const int m0 = mt * MT;
+    if (mt != cur) {
+      __syncthreads();
+      stage_i8_slice<NO, T>(qsm, q8, g.M, C, K, m0);
+      __syncthreads();
+      cur = mt;
+    }
+    const int64_t row = rb * T + threadIdx.x;
+    const bool live = row < g.n;
+    const int64_t rr = live ? row : g.n - 1;
+    int tot[WIDE ? NO * 8 : 1];
+    if constexpr (WIDE) {
+#pragma unroll
+      for (int e = 0; e < NO * 8; ++e) tot[e] = 0;
+    }
+    uint32_t acc[NO][4];  // per 8 columns: bytes {0,2}, {1,3}, {4,6}, {5,7} as u16 pairs
+    RowCodes rc{g.codes + rr * g.code_stride, v16};
+    for (int cb = 0; cb < C; cb += 256) {  // a u16 lane holds <= 256 biased bytes (256 * 255 < 65536)
+      const int ce = min(C, cb + 256);
+#pragma unroll
+      for (int j = 0; j < NO; ++j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[j][i] = 0u;
+      int c0 = cb;
+      if (g.code_bits == 8) {
+        for (; c0 + 16 <= ce; c0 += 16) {
+          const uint4 w = rc.load16(c0);
+          bad |= codes_bad(w, K, pow2);
+#pragma unroll
+          for (int s = 0; s < 16; ++s) {
+            const uint32_t code = code_byte(w, s);
+            i8_lookup<NO>(acc, sbase + (uint32_t)(c0 + s) * cstep, pow2 ? (code & (uint32_t)(K - 1)) : min(code, (uint32_t)(K - 1)), K);
+          }
+        }
+      }
+      for (; c0 < ce; ++c0) {
+        const uint32_t code = (uint32_t)read_code(g, rr, c0);
+        bad |= code >= (uint32_t)K;
+        i8_lookup<NO>(acc, sbase + (uint32_t)c0 * cstep, min(code, (uint32_t)(K - 1)), K);
+      }
+      if constexpr (WIDE) {
+        const int b128 = 128 * (ce - cb);
+#pragma unroll
+        for (int j = 0; j < NO; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            tot[j * 8 + 4 * h + 0] += (int)(acc[j][2 * h] & 0xFFFFu) - b128;
+            tot[j * 8 + 4 * h + 2] += (int)(acc[j][2 * h] >> 16) - b128;
+            tot[j * 8 + 4 * h + 1] += (int)(acc[j][2 * h + 1] & 0xFFFFu) - b128;
+            tot[j * 8 + 4 * h + 3] += (int)(acc[j][2 * h + 1] >> 16) - b128;
           }
       }
+    }
+    if (!live) continue;
+    int64_t obase, ocs;
+    out_row(g, row, obase, ocs);
+    const int b_all = 128 * C;
+    const bool vrow = ocs == 1 && (g.M & 3) == 0;
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        if (rows[r] >= g.n) continue;
-        int64_t base, cs;
-        out_row(g, rows[r], base, cs);
+    for (int j = 0; j < NO; ++j) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int col = col0 + e;
-          if (col >= g.M) continue;
-          const int64_t o = base + (int64_t)col * cs;
-          if (g.out_i32) g.out_i32[o] = tot[r][e];
-          if (g.out) {
-            float f = __fmul_rn(__int2float_rn(tot[r][e]), scale_of(g, col));
-            g.out[o] = f32_epilogue(g, f, col);
-          }
+      for (int h = 0; h < 2; ++h) {  // 4 columns at a time
+        const int col = m0 + 8 * j + 4 * h;
+        int a[4];
+        if constexpr (WIDE) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) a[e] = tot[j * 8 + 4 * h + e];
+        } else {
+          a[0] = (int)(acc[j][2 * h] & 0xFFFFu) - b_all;
+          a[1] = (int)(acc[j][2 * h + 1] & 0xFFFFu) - b_all;
+          a[2] = (int)(acc[j][2 * h] >> 16) - b_all;
+          a[3] = (int)(acc[j][2 * h + 1] >> 16) - b_all;
+        }
+        const bool vec = vrow && col + 3 < g.M;
+        if (g.out_i32) {
+          if (vec && (reinterpret_cast<uintptr_t>(g.out_i32) & 15) == 0)
+            *reinterpret_cast<int4*>(g.out_i32 + obase + col) = make_int4(a[0], a[1], a[2], a[3]);
+          else
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (col + e < g.M) g.out_i32[obase + (int64_t)(col + e) * ocs] = a[e];
+        }
+        if (g.out) {
+          float v[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            v[e] = col + e < g.M ? f32_epilogue(g, __fmul_rn(__int2float_rn(a[e]), scale_of(g, col + e)), col + e)
+                                 : 0.f;
+          if (vec && (reinterpret_cast<uintptr_t>(g.out) & 15) == 0)
+            *reinterpret_cast<float4*>(g.out + obase + col) = make_float4(v[0], v[1], v[2], v[3]);
+          else
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (col + e < g.M) g.out[obase + (int64_t)(col + e) * ocs] = v[e];
         }
       }
     }
   }
+  if (bad && g.err) atomicMax(g.err, (int)LUT_ERR_CORRUPTION);
 }
 
 // ------------------------------------------------------------ host launch
@@ -386,27 +552,37 @@ static int generic_grid(int64_t total) {
   return (int)(b < cap ? (b > 0 ? b : 1) : cap);
 }
 
-template <class T>
-static int launch_tiled(void (*kern)(GatherArgs, const T*), int nmt, size_t smem, const GatherArgs& g,
-                        const T* table, cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+// Grid and band for the row-parallel kernels: as many CTAs as fit (SMEM slice
+// per CTA), at most one per unit; a band of row blocks keeps its codes in L2
+// while each CTA walks ~64 consecutive units of it (so it spans ~2 m-tiles and
+// re-stages its slice ~2-3 times per band).
+template <class T, int TH>
+static int launch_rows(void (*kern)(GatherArgs, const T*, int64_t), int nmt, size_t smem, const GatherArgs& g,
+                       const T* table, cudaStream_t stream) {
+  cudaError_t e = kernel_smem_attr(reinterpret_cast<const void*>(kern));
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(gather)");
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGatherThreads, smem);
-  if (per_sm < 1) per_sm = 1;
-  const int slots = num_sms() * per_sm;
-  // CTAs per m-tile: each re-stages its m-tile's table slice, so with few rows cap
-  // the split at ~min_rows rows per CTA (LUTGPU_GATHER_MINROWS; 0 = no cap)
-  int64_t min_rows = 256;
-  if (const char* e = probe_env("LUTGPU_GATHER_MINROWS")) min_rows = atoll(e);
-  int cpm = nmt >= slots ? 1 : slots / nmt;
-  if (min_rows > 0) {
-    const int64_t cap = (g.n + min_rows - 1) / min_rows;
-    if (cap < cpm) cpm = (int)(cap > 0 ? cap : 1);
-  }
-  int grid = nmt >= slots ? slots : cpm * nmt;
-  kern<<<grid, kGatherThreads, smem, stream>>>(g, table);
+  const int per_sm = kernel_occupancy(reinterpret_cast<const void*>(kern), TH, smem);
+  const int64_t nrb = (g.n + TH - 1) / TH;
+  const int64_t units = nrb * nmt;
+  const int64_t slots = (int64_t)num_sms() * per_sm;
+  const int grid = (int)(units < slots ? units : slots);
+  int64_t band_rb = (64 * (int64_t)grid + nmt - 1) / nmt;
+  const int64_t code_row_bytes = g.code_stride > 0 ? g.code_stride : g.C;
+  const int64_t max_band = ((int64_t)32 << 20) / (TH * code_row_bytes + 1);
+  if (band_rb > max_band) band_rb = max_band;
+  if (band_rb < 1) band_rb = 1;
+  if (band_rb > nrb) band_rb = nrb;
+  kern<<<grid, TH, smem, stream>>>(g, table, band_rb);
   return LUT_OK;
+}
+
+// Rows per CTA: 512 (16 warps hide the LDS latency) unless that leaves SMs idle.
+static bool small_rows(int64_t n, int nmt) { return (n + 511) / 512 * (int64_t)nmt < 2 * (int64_t)num_sms(); }
+
+template <int NP>
+static int launch_f32(int nmt, size_t smem, const GatherArgs& g, const float* table, cudaStream_t stream, bool small) {
+  return small ? launch_rows<float, 128>(gather_f32_rows<NP, 128>, nmt, smem, g, table, stream)
+               : launch_rows<float, 512>(gather_f32_rows<NP, 512>, nmt, smem, g, table, stream);
 }
 
 int gather_f32_strided(const uint8_t* codes, int code_bits, int64_t code_stride, int64_t n, int C, int K, int M,
@@ -416,42 +592,44 @@ int gather_f32_strided(const uint8_t* codes, int code_bits, int64_t code_stride,
   GatherArgs g = make_args(codes, code_bits, n, C, K, M, bias, act, out, nullptr, out_hw, err);
   g.code_stride = code_stride;
   const size_t budget = 200 * 1024;
-  const size_t per_col = (size_t)C * K * sizeof(float);
-  int MT = 0;
-  // m-tile width: the widest slice that fits; with few rows prefer narrower
-  // slices (more m-tiles, each CTA stages less) until the m-tiles fill the chip
-  int mt_cap = 64;
-  if (const char* e = probe_env("LUTGPU_GATHER_MT")) mt_cap = atoi(e);
-  else if (n < 65536) {
-    const int floor_mt = n < 16384 ? 8 : 16;
-    while (mt_cap > floor_mt && (M + mt_cap - 1) / mt_cap < num_sms()) mt_cap /= 2;
-  }
+  const size_t per_chunk = (size_t)C * K * 8;  // SMEM bytes per 2-column chunk
+  int NP = 0;
   if (!force_generic && C > 0) {
-    for (int cand : {64, 32, 16, 8, 4}) {
-      if (cand <= mt_cap && per_col * cand <= budget && (cand <= 4 || (M + 3) / 4 * 4 >= cand)) {
-        MT = cand;
+    for (int cand : {8, 4, 2, 1})
+      if (per_chunk * cand <= budget) {
+        NP = cand;
         break;
       }
-    }
+    while (NP > 1 && 2 * (NP / 2) >= M) NP /= 2;  // do not stage columns beyond M
   }
-  if (MT == 0) {
+  if (NP == 0) {
     gather_f32_generic<<<generic_grid(n * M), 256, 0, stream>>>(g, table);
     LUT_CHECK_LAUNCH("gather_f32_generic");
     return LUT_OK;
   }
-  const int nmt = (M + MT - 1) / MT;
-  const size_t smem = per_col * MT;
+  int nmt = (M + 2 * NP - 1) / (2 * NP);
+  bool small = small_rows(n, nmt);
+  while (small && NP > 1 && (n + 127) / 128 * (int64_t)nmt < num_sms()) {  // few rows: narrower slices, more units
+    NP /= 2;
+    nmt = (M + 2 * NP - 1) / (2 * NP);
+  }
+  const size_t smem = per_chunk * NP;
   int st = LUT_OK;
-  switch (MT) {
-    case 64: st = launch_tiled(gather_f32_tiled<64>, nmt, smem, g, table, stream); break;
-    case 32: st = launch_tiled(gather_f32_tiled<32>, nmt, smem, g, table, stream); break;
-    case 16: st = launch_tiled(gather_f32_tiled<16>, nmt, smem, g, table, stream); break;
-    case 8: st = launch_tiled(gather_f32_tiled<8>, nmt, smem, g, table, stream); break;
-    default: st = launch_tiled(gather_f32_tiled<4>, nmt, smem, g, table, stream); break;
+  switch (NP) {
+    case 8: st = launch_f32<8>(nmt, smem, g, table, stream, small); break;
+    case 4: st = launch_f32<4>(nmt, smem, g, table, stream, small); break;
+    case 2: st = launch_f32<2>(nmt, smem, g, table, stream, small); break;
+    default: st = launch_f32<1>(nmt, smem, g, table, stream, small); break;
   }
   if (st != LUT_OK) return st;
-  LUT_CHECK_LAUNCH("gather_f32_tiled");
+  LUT_CHECK_LAUNCH("gather_f32_rows");
   return LUT_OK;
+}
+
+template <int NO, bool WIDE>
+static int launch_i8(int nmt, size_t smem, const GatherArgs& g, const int8_t* q, cudaStream_t stream, bool small) {
+  return small ? launch_rows<int8_t, 128>(gather_i8_rows<NO, WIDE, 128>, nmt, smem, g, q, stream)
+               : launch_rows<int8_t, 512>(gather_i8_rows<NO, WIDE, 512>, nmt, smem, g, q, stream);
 }
 
 int gather_i8_strided(const uint8_t* codes, int code_bits, int64_t code_stride, int64_t n, int C, int K, int M,
@@ -463,32 +641,41 @@ int gather_i8_strided(const uint8_t* codes, int code_bits, int64_t code_stride, 
   g.scales = scales;
   g.scale_mtile = scale_mtile;
   const size_t budget = 200 * 1024;
-  const size_t per_col = (size_t)C * K;
-  int MT = 0;
+  const size_t per_chunk = (size_t)C * K * 8;  // SMEM bytes per 8-column chunk
+  const bool wide = C > 256;
+  int NO = 0;
   if (!force_generic && C > 0) {
-    for (int cand : {128, 64, 32, 16}) {
-      if (per_col * cand <= budget && (cand <= 16 || (M + 15) / 16 * 16 >= cand)) {
-        MT = cand;
+    for (int cand : {4, 2, 1})
+      if (per_chunk * cand <= budget && !(wide && cand > 2)) {
+        NO = cand;
         break;
       }
-    }
+    while (NO > 1 && 8 * (NO / 2) >= M) NO /= 2;  // do not stage columns beyond M
   }
-  if (MT == 0) {
+  if (NO == 0) {
     gather_i8_generic<<<generic_grid(n * M), 256, 0, stream>>>(g, q);
     LUT_CHECK_LAUNCH("gather_i8_generic");
     return LUT_OK;
   }
-  const int nmt = (M + MT - 1) / MT;
-  const size_t smem = per_col * MT;
+  int nmt = (M + 8 * NO - 1) / (8 * NO);
+  bool small = small_rows(n, nmt);
+  while (small && NO > 1 && (n + 127) / 128 * (int64_t)nmt < num_sms()) {
+    NO /= 2;
+    nmt = (M + 8 * NO - 1) / (8 * NO);
+  }
+  const size_t smem = per_chunk * NO;
   int st = LUT_OK;
-  switch (MT) {
-    case 128: st = launch_tiled(gather_i8_tiled<128>, nmt, smem, g, q, stream); break;
-    case 64: st = launch_tiled(gather_i8_tiled<64>, nmt, smem, g, q, stream); break;
-    case 32: st = launch_tiled(gather_i8_tiled<32>, nmt, smem, g, q, stream); break;
-    default: st = launch_tiled(gather_i8_tiled<16>, nmt, smem, g, q, stream); break;
+  if (wide) {
+    st = NO == 2 ? launch_i8<2, true>(nmt, smem, g, q, stream, small) : launch_i8<1, true>(nmt, smem, g, q, stream, small);
+  } else {
+    switch (NO) {
+      case 4: st = launch_i8<4, false>(nmt, smem, g, q, stream, small); break;
+      case 2: st = launch_i8<2, false>(nmt, smem, g, q, stream, small); break;
+      default: st = launch_i8<1, false>(nmt, smem, g, q, stream, small); break;
+    }
   }
   if (st != LUT_OK) return st;
-  LUT_CHECK_LAUNCH("gather_i8_tiled");
+  LUT_CHECK_LAUNCH("gather_i8_rows");
   return LUT_OK;
 }
 

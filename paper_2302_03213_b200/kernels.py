@@ -250,9 +250,14 @@ def lut_gather_accumulate(enc, table: LookupTableI8, plan: KernelPlan = KernelPl
     kind = D.kind_of(enc)
     dev = D.require_cuda()
     codes = _codes_device(enc, c, k, dev)
-    q_dev = D.to_device(table.q, np.int8, dev)
     err = D.ErrFlag(dev)
-    out = _gather_i8_f32(codes, q_dev, table.scales_tensor(dev), table.scale_mtile, None, 0, c, k, m, err.p)
+    if getattr(table, "per_codebook", False):  # extension: f32 sum of the dequantized entries
+        from .quant import dequantized_table
+
+        out = _gather_f32(codes, dequantized_table(table, dev), None, 0, c, k, m, err.p)
+    else:
+        q_dev = D.to_device(table.q, np.int8, dev)
+        out = _gather_i8_f32(codes, q_dev, table.scales_tensor(dev), table.scale_mtile, None, 0, c, k, m, err.p)
     check(load().lut_read_status(err.p, D.stream_ptr()), "lut_gather_accumulate")
     return D.from_device(out, kind)
 

@@ -40,7 +40,7 @@ class LutLayer:
 
     def __init__(self, cfg: PqConfig, books, weight=None, bias=None, qat: bool = False, table=None,
                  qtable: LookupTableI8 | None = None, trees=None, act=None, scale_mtile: int = 0,
-                 device=None, gather: str = "auto", f32_digits: int = 4):
+                 device=None, gather: str = "auto", f32_digits: int = 4, scale_per_codebook: bool = False):
         """`gather` picks the lookup engine: "cuda" = CUDA-core kernels (f32
         bitwise ascending-c, int8 exact); "tensor" = tcgen05 one-hot GEMM (int8
         exact; f32 as `f32_digits` int8 digit planes, within the fp32
@@ -65,6 +65,8 @@ class LutLayer:
         self.trees = trees
         self.act = act
         self.scale_mtile = scale_mtile
+        self.scale_per_codebook = scale_per_codebook
+        self._deq = None
         self.books = D.to_device(books, F32, self.device)
         self.books_prep = prepare_books(self.books)
         self.weight = None
@@ -83,7 +85,8 @@ class LutLayer:
                                         else torch.as_tensor(np.asarray(qtable.scale, F32).reshape(-1),
                                                              device=self.device),
                                         scale_mtile=getattr(qtable, "scale_mtile", 0),
-                                        validated=isinstance(qtable, LookupTableI8))
+                                        validated=isinstance(qtable, LookupTableI8),
+                                        per_codebook=getattr(qtable, "per_codebook", False))
         if self.table is None and self.qtable is None:
             self.rebuild()
         m = self.m
@@ -131,7 +134,8 @@ class LutLayer:
                 raise ConfigError("layer has neither a weight matrix nor a table")
             return
         self.table = build_table_device(self.weight, self.books)
-        self.qtable = quantize_table(self.table, self.scale_mtile) if self.qat else None
+        self.qtable = quantize_table(self.table, self.scale_mtile, self.scale_per_codebook) if self.qat else None
+        self._deq = None
         self._desc_cache = {}
         self._images = {}
         self.__dict__.pop("_act_twins", None)
@@ -140,7 +144,7 @@ class LutLayer:
         """Table the training forward reads: dequantized under QAT (softpq.py:134-140)."""
         if self.qat:
             if self.qtable is None:
-                self.qtable = quantize_table(self.table, self.scale_mtile)
+                self.qtable = quantize_table(self.table, self.scale_mtile, self.scale_per_codebook)
             return dequantize(self.qtable)
         return self.table
 
@@ -148,7 +152,8 @@ class LutLayer:
         """Build (or rebuild) the int8 twin from the f32 table."""
         if scale_mtile is not None:
             self.scale_mtile = scale_mtile
-        self.qtable = quantize_table(self.table, self.scale_mtile)
+        self.qtable = quantize_table(self.table, self.scale_mtile, self.scale_per_codebook)
+        self._deq = None
         self._desc_cache = {}
         self._images.pop(1, None)
         self.__dict__.pop("_act_twins", None)
@@ -172,9 +177,24 @@ class LutLayer:
         return twin
 
     # ---------------------------------------------------------------- ABI
+    @property
+    def per_codebook_scales(self) -> bool:
+        return self.qtable is not None and getattr(self.qtable, "per_codebook", False)
+
+    def dequantized(self) -> torch.Tensor:
+        """fl(q * scale) as an f32 (C, K, M) table: the lookup table of the
+        per-(codebook, m-tile) scale extension (one f32 product per entry)."""
+        if self._deq is None:
+            from .quant import dequantized_table
+
+            self._deq = dequantized_table(self.qtable, self.device)
+        return self._deq
+
     def uses_tensor_cores(self, integer: bool) -> bool:
         if self.gather == "cuda":
             return False
+        if integer and self.per_codebook_scales:
+            return False  # scales differ per codebook: no single exact integer sum to put on the MMA
         if self.gather == "auto" and not integer:
             return False
         digits = 1 if integer else self.f32_digits
@@ -217,6 +237,11 @@ class LutLayer:
         d.bias = D.ptr(self.bias)
         d.act = ACTS[self.act]
         d.integer = 1 if integer else 0
+        if integer and self.per_codebook_scales:
+            # per-(codebook, m-tile) scales: sum the dequantized entries in f32,
+            # ascending c (oracle lut_gather_accumulate_cmtile)
+            d.table = D.ptr(self.dequantized())
+            d.integer = 0
         if self.uses_tensor_cores(integer):
             d.onehot_image = D.ptr(self.onehot_image(integer))
             d.onehot_digits = 1 if integer else self.f32_digits
@@ -290,7 +315,9 @@ class LutLayer:
         # leaves are data: a code >= K raises CorruptionError like lut_gather_i32 /
         # lut_matmul_ref (kernels.py:117-118, pq.py:209-210), never a clamp
         err = D.ErrFlag(self.device)
-        if integer:
+        if integer and self.per_codebook_scales:
+            out = _gather_f32(codes, self.dequantized(), self.bias, act, self.c, self.k, self.m, err.p)
+        elif integer:
             out = _gather_i8_f32(codes, self.qtable.q, self.qtable.scales_tensor(self.device), self.qtable.scale_mtile,
                                  self.bias, act, self.c, self.k, self.m, err.p)
         else:

@@ -90,13 +90,15 @@ def conv_forward(x, lut: LutLayer, cin: int, kernel: int, stride: int, pad: int,
                                     lut.qtable.scale_mtile if integer else 0, D.ptr(lut.bias), act, D.ptr(out),
                                     None, ho * wo, D.stream_ptr()), "LutConv")
     else:
-        err = D.ErrFlag(dev)
-        if integer:
+        # codes come from the distance encoder, so they are < K by construction: no
+        # error flag (and no stream sync: the layer stays capturable in a CUDA graph)
+        if integer and lut.per_codebook_scales:
+            _gather_f32(codes, lut.dequantized(), lut.bias, act, lut.c, lut.k, lut.m, None, out_hw=ho * wo, out=out)
+        elif integer:
             _gather_i8_f32(codes, lut.qtable.q, lut.qtable.scales_tensor(dev), lut.qtable.scale_mtile, lut.bias,
-                           act, lut.c, lut.k, lut.m, err.p, out_hw=ho * wo, out=out)
+                           act, lut.c, lut.k, lut.m, None, out_hw=ho * wo, out=out)
         else:
-            _gather_f32(codes, lut.table, lut.bias, act, lut.c, lut.k, lut.m, err.p, out_hw=ho * wo, out=out)
-        check(lib.lut_read_status(err.p, D.stream_ptr()), "LutConv")
+            _gather_f32(codes, lut.table, lut.bias, act, lut.c, lut.k, lut.m, None, out_hw=ho * wo, out=out)
     return D.from_device(out, kind)
 
 

@@ -51,11 +51,11 @@ def sample_centroids(held: torch.Tensor, v: int, k: int, gen: torch.Generator) -
 
 
 def lut_from_dense(weight_dm: torch.Tensor, bias, held: torch.Tensor, v: int, k: int, gen, integer=True,
-                   act=None, scale_mtile: int = 0, gather: str = "auto") -> LutLayer:
+                   act=None, scale_mtile: int = 0, gather: str = "auto", per_codebook: bool = False) -> LutLayer:
     """Replace a (D, M) weight by a LUT layer whose centroids come from `held`."""
     books = sample_centroids(held, v, k, gen)
     return LutLayer(cfg=PqConfig(v=v, k=k), books=books, weight=weight_dm, bias=bias, qat=integer, act=act,
-                    scale_mtile=scale_mtile, device=weight_dm.device, gather=gather)
+                    scale_mtile=scale_mtile, device=weight_dm.device, gather=gather, scale_per_codebook=per_codebook)
 
 
 def standardize(x: torch.Tensor, eps: float = 1e-5) -> torch.Tensor:
@@ -93,17 +93,21 @@ class FfnPair(torch.nn.Module):
 
 
 def ffn_pair(dev, tokens: int = 4096, hidden: int = 768, ffn: int = 3072, v: int = 32, k: int = 16,
-             scale_mtile: int = 0, seed: int = 2024, held_rows: int = 4096, gather: str = "auto"):
+             scale_mtile: int = 0, seed: int = 2024, held_rows: int = 4096, gather: str = "auto",
+             per_codebook: bool = False):
     """configs[1]: inputs standardised N(0,1); W ~N(0, 0.02); centroids from a
     held-out batch (FFN2's from GELU(FFN1) of that batch, dense); int8 tables,
-    one scale per table (parity) or per m-tile (`scale_mtile`, extension)."""
+    one scale per table (parity), per m-tile (`scale_mtile`) or per (codebook,
+    m-tile) (`per_codebook`, BASELINE's wording; extensions)."""
     g = _gen(dev, seed)
     w1 = torch.randn((hidden, ffn), generator=g, device=dev) * 0.02
     w2 = torch.randn((ffn, hidden), generator=g, device=dev) * 0.02
     held = standardize(torch.randn((held_rows, hidden), generator=g, device=dev))
-    up = lut_from_dense(w1, None, held, v, k, g, act="gelu", scale_mtile=scale_mtile, gather=gather)
+    up = lut_from_dense(w1, None, held, v, k, g, act="gelu", scale_mtile=scale_mtile, gather=gather,
+                        per_codebook=per_codebook)
     held2 = F.gelu(_mm(held, w1))
-    down = lut_from_dense(w2, None, held2, v, k, g, scale_mtile=scale_mtile, gather=gather)
+    down = lut_from_dense(w2, None, held2, v, k, g, scale_mtile=scale_mtile, gather=gather,
+                          per_codebook=per_codebook)
     x = standardize(torch.randn((tokens, hidden), generator=_gen(dev, seed + 1), device=dev))
     return FfnPair(up, down), x
 
