@@ -529,6 +529,42 @@ struct ConvPlaneParams {
   uint32_t slot_bytes;   // 8 planes, 128-aligned
 };
 
+// Best / second-best / lowest-index argmin of 2*KP distances held as
+// (2k, 2k+1) pairs, as a log-depth tree: a sequential scan is a 3-op dependent
+// chain per centroid, which with 8 warps per SM left the kernel latency-bound.
+// Ties keep the lower index (strict < when the higher-index half wins), the
+// reference's np.argmin rule; equal best values give second == best, i.e. an
+// exact tie that the caller re-decides in f64.
+template <int KP>
+__device__ __forceinline__ void argmin_tree(const uint64_t (&acc)[KP], float& best_out, float& second_out,
+                                            int& idx_out) {
+  float b[KP], s2[KP];
+  int ix[KP];
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    float d0, d1;
+    unpack_f2(acc[k], d0, d1);
+    const bool pk = d1 < d0;
+    b[k] = fminf(d0, d1);
+    s2[k] = fmaxf(d0, d1);
+    ix[k] = pk ? 2 * k + 1 : 2 * k;
+  }
+#pragma unroll
+  for (int w = 1; w < KP; w *= 2) {
+#pragma unroll
+    for (int k = 0; k + w < KP; k += 2 * w) {
+      const bool pk = b[k + w] < b[k];  // right (higher indices) wins only strictly
+      const float hi = fmaxf(b[k], b[k + w]);
+      s2[k] = fminf(hi, pk ? s2[k + w] : s2[k]);
+      b[k] = fminf(b[k], b[k + w]);
+      ix[k] = pk ? ix[k + w] : ix[k];
+    }
+  }
+  best_out = b[0];
+  second_out = s2[0];
+  idx_out = ix[0];
+}
+
 template <int K, int KH>
 __global__ void __launch_bounds__(kConvWarps * 32, 1) encode_conv_plane_kernel(ConvPlaneParams p) {
   constexpr int V = KH * KH;
@@ -625,19 +661,9 @@ __global__ void __launch_bounds__(kConvWarps * 32, 1) encode_conv_plane_kernel(C
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          float best = FLT_MAX, second = FLT_MAX;
-          int bi = 0;
-#pragma unroll
-          for (int k = 0; k < KP; ++k) {
-            float d0, d1;
-            unpack_f2(acc[r][k], d0, d1);
-            second = fminf(second, fmaxf(best, d0));
-            bi = (d0 < best) ? 2 * k : bi;
-            best = fminf(best, d0);
-            second = fminf(second, fmaxf(best, d1));
-            bi = (d1 < best) ? 2 * k + 1 : bi;
-            best = fminf(best, d1);
-          }
+          float best, second;
+          int bi;
+          argmin_tree<KP>(acc[r], best, second, bi);
           if (pixr[r] < hw_out) {
             if (!(second - best > tau_c * (asq[r] + pmax))) {
               const int H = p.h, W = p.w, yy = y0[r], xx = x0[r];
