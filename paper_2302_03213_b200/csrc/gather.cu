@@ -222,6 +222,20 @@ __device__ __forceinline__ void stage_f32_slice(uint2* tsm, const float* __restr
   const int total = C * K * NP;
   const bool vec = (M & 1) == 0 && (reinterpret_cast<uintptr_t>(table) & 7) == 0;
   const int lk = (K & (K - 1)) == 0 ? __ffs(K) - 1 : -1;
+  if (vec && m0 + 2 * NP <= M) {
+    // every 8-byte pair in flight at once (cp.async, no register staging): the
+    // slice costs one L2 / HBM round trip instead of one per load batch
+    const uint32_t sbase = smem_u32(tsm);
+    for (int i = threadIdx.x; i < total; i += T) {
+      const int ck = i / NP, j = i - ck * NP;
+      const int c = lk >= 0 ? ck >> lk : ck / K, k = ck - c * K;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sbase + (uint32_t)(((c * NP + j) * K + k) * 8)),
+                   "l"(table + (int64_t)ck * M + m0 + 2 * j)
+                   : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
   for (int base = threadIdx.x; base < total; base += 8 * T) {
     uint2 v[8];
 #pragma unroll
@@ -258,6 +272,24 @@ __device__ __forceinline__ void stage_i8_slice(uint2* qsm, const int8_t* __restr
   const int total = C * K * NO;
   const bool vec = (M & 7) == 0 && (reinterpret_cast<uintptr_t>(q8) & 7) == 0;
   const int lk = (K & (K - 1)) == 0 ? __ffs(K) - 1 : -1;
+  if (vec && m0 + 8 * NO <= M) {
+    // all 8-byte chunks in flight (cp.async), then bias them in place
+    const uint32_t sbase = smem_u32(qsm);
+    for (int i = threadIdx.x; i < total; i += T) {
+      const int ck = i / NO, j = i - ck * NO;
+      const int c = lk >= 0 ? ck >> lk : ck / K, k = ck - c * K;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sbase + (uint32_t)(((c * NO + j) * K + k) * 8)),
+                   "l"(q8 + (int64_t)ck * M + m0 + 8 * j)
+                   : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    for (int i = threadIdx.x; i < total; i += T) {
+      const uint2 w = qsm[i];
+      qsm[i] = make_uint2(w.x ^ 0x80808080u, w.y ^ 0x80808080u);
+    }
+    return;
+  }
   for (int base = threadIdx.x; base < total; base += 8 * T) {
     uint2 v[8];
 #pragma unroll
@@ -609,7 +641,9 @@ int gather_f32_strided(const uint8_t* codes, int code_bits, int64_t code_stride,
   }
   int nmt = (M + 2 * NP - 1) / (2 * NP);
   bool small = small_rows(n, nmt);
-  while (small && NP > 1 && (n + 127) / 128 * (int64_t)nmt < num_sms()) {  // few rows: narrower slices, more units
+  // few rows: narrower slices and more CTAs until every SM holds several (the
+  // per-row lookup chains are latency-bound at 2 warps per scheduler)
+  while (small && NP > 1 && (n + 127) / 128 * (int64_t)nmt < 4 * (int64_t)num_sms()) {
     NP /= 2;
     nmt = (M + 2 * NP - 1) / (2 * NP);
   }
@@ -659,7 +693,7 @@ int gather_i8_strided(const uint8_t* codes, int code_bits, int64_t code_stride, 
   }
   int nmt = (M + 8 * NO - 1) / (8 * NO);
   bool small = small_rows(n, nmt);
-  while (small && NO > 1 && (n + 127) / 128 * (int64_t)nmt < num_sms()) {
+  while (small && NO > 1 && (n + 127) / 128 * (int64_t)nmt < 4 * (int64_t)num_sms()) {
     NO /= 2;
     nmt = (M + 8 * NO - 1) / (8 * NO);
   }
