@@ -906,6 +906,10 @@ int encode_dense(const float* a, int64_t n, int d, const float* prep, int C, int
   return launch_rows(&rows, nullptr, n, prep, C, K, V, codes, code_bits, code_stride, near_tie, stream);
 }
 
+int launch_conv_tc(const float* x, int batch, int cin, int h, int w, int stride, int pad, int ho, int wo,
+                   const float* prep, int K, uint8_t* codes, int64_t code_stride, int* near_tie, cudaStream_t stream,
+                   bool* used);
+
 int encode_conv(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad,
                 const float* prep, int C, int K, int V, uint8_t* codes, int code_bits, int* near_tie,
                 cudaStream_t stream) {
@@ -918,6 +922,14 @@ int encode_conv(const float* x, int batch, int cin, int h, int w, int kh, int kw
   if (code_bits == 8 && kh == 3 && kw == 3 && V == 9 && C == cin && !(force && atoi(force))) {
     bool used = false;
     int st = LUT_OK;
+    const char* tc_env = probe_env("LUTGPU_CONV_TC");
+    if (K == 16 && !(tc_env && tc_env[0] == '0')) {
+      // tensor-core screening (encode_conv_tc.cu)
+      st = launch_conv_tc(x, batch, cin, h, w, stride, pad, ho, wo, prep, K, codes, code_stride, near_tie, stream,
+                          &used);
+      if (st != LUT_OK) return st;
+      if (used) return LUT_OK;
+    }
     if (K == 16)
       st = launch_conv_plane<16, 3>(x, batch, cin, h, w, stride, pad, ho, wo, prep, codes, code_stride, near_tie,
                                     stream, &used);

@@ -325,7 +325,7 @@ __device__ __forceinline__ void stage_i8_slice(uint2* qsm, const int8_t* __restr
 
 // Thread block of T threads; NP chunks of 2 f32 columns per thread (MT = 2 * NP).
 template <int NP, int T>
-__global__ void __launch_bounds__(T, 1)
+__global__ void __launch_bounds__(T, T <= 128 ? 4 : 1)
     gather_f32_rows(GatherArgs g, const float* __restrict__ table, int64_t band_rb) {
   extern __shared__ uint2 tsm[];  // [C][NP][K] float pairs
   constexpr int MT = 2 * NP;
@@ -359,8 +359,12 @@ __global__ void __launch_bounds__(T, 1)
     if (g.code_bits == 8) {
       RowCodes rc{g.codes + rr * g.code_stride, v16};
       int c0 = 0;
+      // the next 16 codes are loaded while the current 16 are looked up (a
+      // load-then-use loop serialises one global latency per 16 codebooks)
+      uint4 wn = C >= 16 ? rc.load16(0) : make_uint4(0u, 0u, 0u, 0u);
       for (; c0 + 16 <= C; c0 += 16) {
-        const uint4 w = rc.load16(c0);
+        const uint4 w = wn;
+        if (c0 + 32 <= C) wn = rc.load16(c0 + 16);
         bad |= codes_bad(w, K, pow2);
 #pragma unroll
         for (int s = 0; s < 16; ++s) {
@@ -435,7 +439,7 @@ __device__ __forceinline__ void i8_lookup(uint32_t (&acc)[NO][4], uint32_t cbase
 // int8: NO chunks of 8 columns per thread (MT = 8 * NO); biased bytes (q + 128)
 // summed as u16 pairs, widened every 256 codebooks when WIDE.
 template <int NO, bool WIDE, int T>
-__global__ void __launch_bounds__(T, 1)
+__global__ void __launch_bounds__(T, T <= 128 ? 4 : 1)
     gather_i8_rows(GatherArgs g, const int8_t* __restrict__ q8, int64_t band_rb) {
   extern __shared__ uint2 qsm[];  // [C][NO][K] x 8 biased bytes
   constexpr int MT = 8 * NO;
@@ -478,8 +482,10 @@ __global__ void __launch_bounds__(T, 1)
         for (int i = 0; i < 4; ++i) acc[j][i] = 0u;
       int c0 = cb;
       if (g.code_bits == 8) {
+        uint4 wn = c0 + 16 <= ce ? rc.load16(c0) : make_uint4(0u, 0u, 0u, 0u);
         for (; c0 + 16 <= ce; c0 += 16) {
-          const uint4 w = rc.load16(c0);
+          const uint4 w = wn;  // next 16 codes in flight during these lookups
+          if (c0 + 32 <= ce) wn = rc.load16(c0 + 16);
           bad |= codes_bad(w, K, pow2);
 #pragma unroll
           for (int s = 0; s < 16; ++s) {
