@@ -277,7 +277,7 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
         float mn = fminf(fminf(dt[0], dt[1]), fminf(dt[2], dt[3]));
 #pragma unroll
         for (int k = 4; k < 16; k += 4) mn = fminf(mn, fminf(fminf(dt[k], dt[k + 1]), fminf(dt[k + 2], dt[k + 3])));
-#pragma unroll 1
+#pragma unroll
         for (int kc = 16; kc < NK; kc += 16) {  // K = 64: the other 16-column chunks (minimum pass)
           uint32_t dw[16];
           tc_ld16(dslot + (uint32_t)kc, dw);
@@ -292,17 +292,21 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
           }
         }
         const float thr = __fadd_ru(mn, 2.0f * hw);
-        MaskT mask = 0;
+        // candidate bits per 16-column chunk in 32-bit registers (constant shifts:
+        // the chunk loops are unrolled), merged into the K-bit mask once per chunk
+        uint32_t m16 = 0u;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) mask |= (dt[k] <= thr) ? ((MaskT)1 << k) : (MaskT)0;
-#pragma unroll 1
+        for (int k = 0; k < 16; ++k) m16 |= (dt[k] <= thr) ? (1u << k) : 0u;
+        MaskT mask = (MaskT)m16;
+#pragma unroll
         for (int kc = 16; kc < NK; kc += 16) {  // K = 64: candidate pass (same fp32 expression)
           uint32_t dw[16];
           tc_ld16(dslot + (uint32_t)kc, dw);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          uint32_t mc = 0u;
 #pragma unroll
-          for (int k = 0; k < 16; ++k)
-            mask |= (fmaf(-2.0f, __uint_as_float(dw[k]), pn[kc + k]) <= thr) ? ((MaskT)1 << (kc + k)) : (MaskT)0;
+          for (int k = 0; k < 16; ++k) mc |= (fmaf(-2.0f, __uint_as_float(dw[k]), pn[kc + k]) <= thr) ? (1u << k) : 0u;
+          mask |= (MaskT)mc << kc;
         }
         int code;
         if ((mask & (mask - 1)) == 0 && mask != 0) {
