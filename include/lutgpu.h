@@ -234,6 +234,18 @@ LUT_API int lut_layer_forward(const lut_layer_desc* layer, const float* a, int64
                       uint8_t* codes_scratch, int32_t* near_tie_count, lut_stream_t stream);
 
 /*
+ * Full conv layer (LutConv.forward, model.py:199-203 with Conv._lower/_raise,
+ * model.py:105-114): NCHW input x (batch, cin, h, w) -> encode of every
+ * kh x kw patch (im2col fused, tensor.py:36-79) -> lookup-aggregate -> bias/act
+ * -> NCHW output (batch, m, ho, wo).  codes_scratch: batch*ho*wo *
+ * lut_code_stride(c) bytes.  The lookup is launched as a programmatic dependent
+ * of the encode (it stages its table slice while the encode finishes).
+ */
+LUT_API int lut_conv_layer_forward(const lut_layer_desc* layer, const float* x, int32_t batch, int32_t cin,
+                                   int32_t h, int32_t w, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
+                                   float* out, uint8_t* codes_scratch, int32_t* near_tie_count, lut_stream_t stream);
+
+/*
  * Host-memory executor: the same layer over HOST rows.  Streams row chunks
  * host->device, runs lut_layer_forward, and streams results device->host, with
  * copies and compute overlapped on three streams (copy-in, compute, copy-out)

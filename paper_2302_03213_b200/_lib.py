@@ -60,6 +60,7 @@ SIGNATURES = {
     "lut_onehot_prepare_f32": (C.c_int, [P, I32, I32, I32, I32, P, P, P]),
     "lut_gather_onehot": (C.c_int, [P, I64, I64, I32, I32, I32, I32, P, P, I32, P, I32, P, P, I64, P]),
     "lut_code_stride": (I64, [I32]),
+    "lut_conv_layer_forward": (C.c_int, [C.POINTER(LayerDesc), P, I32, I32, I32, I32, I32, I32, I32, I32, P, P, P, P]),
     "lut_layer_forward": (C.c_int, [C.POINTER(LayerDesc), P, I64, P, P, P, P]),
     "lut_pipeline_create": (C.c_int, [I32, I64, I32, I32, I32, C.POINTER(C.c_void_p)]),
     "lut_pipeline_run": (C.c_int, [P, C.POINTER(LayerDesc), P, I64, P, c_int32_p]),

@@ -42,6 +42,9 @@ int onehot_prepare_f32(const float* t, int C, int K, int M, int digits, void* im
 int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, int K, int M, int digits,
                   const void* image, const float* scales, int scale_mtile, const float* bias, int act, float* out,
                   int32_t* out_i32, int64_t out_hw, cudaStream_t stream);
+int encode_conv_strided(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad,
+                        const float* prep, int C, int K, int V, uint8_t* codes, int64_t code_stride, int* near_tie,
+                        cudaStream_t stream);
 int encode_conv(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad,
                 const float* prep, int C, int K, int V, uint8_t* codes, int code_bits, int* near_tie,
                 cudaStream_t stream);
@@ -57,10 +60,10 @@ int gather_i8(const uint8_t* codes, int code_bits, int64_t n, int C, int K, int 
               int64_t out_hw, int* err, cudaStream_t stream, int force_generic);
 int gather_f32_strided(const uint8_t* codes, int code_bits, int64_t code_stride, int64_t n, int C, int K, int M,
                        const float* table, const float* bias, int act, float* out, int64_t out_hw, int* err,
-                       cudaStream_t stream, int force_generic);
+                       cudaStream_t stream, int force_generic, int pdl = 0);
 int gather_i8_strided(const uint8_t* codes, int code_bits, int64_t code_stride, int64_t n, int C, int K, int M,
                       const int8_t* q, const float* scales, int scale_mtile, const float* bias, int act, float* out,
-                      int32_t* out_i32, int64_t out_hw, int* err, cudaStream_t stream, int force_generic);
+                      int32_t* out_i32, int64_t out_hw, int* err, cudaStream_t stream, int force_generic, int pdl = 0);
 int build_table(const float* b, int M, const float* books, int C, int K, int V, float* table,
                 cudaStream_t stream);
 size_t quantize_scratch_bytes(int C, int K, int M, int mtile);
@@ -462,9 +465,38 @@ int lut_layer_forward(const lut_layer_desc* L, const float* a, int64_t n, float*
   }
   if (L->integer)
     return gather_i8_strided(codes_scratch, 8, stride, n, L->c, L->k, L->m, L->q, L->scales, L->scale_mtile, L->bias,
-                             L->act, out, nullptr, 0, nullptr, s, force_generic_env());
+                             L->act, out, nullptr, 0, nullptr, s, force_generic_env(), /*pdl=*/1);
   return gather_f32_strided(codes_scratch, 8, stride, n, L->c, L->k, L->m, L->table, L->bias, L->act, out, 0, nullptr,
-                            s, force_generic_env());
+                            s, force_generic_env(), /*pdl=*/1);
+}
+
+int lut_conv_layer_forward(const lut_layer_desc* L, const float* x, int32_t batch, int32_t cin, int32_t h, int32_t w,
+                           int32_t kh, int32_t kw, int32_t stride, int32_t pad, float* out, uint8_t* codes_scratch,
+                           int32_t* near_tie_count, lut_stream_t stream) {
+  LUT_TRY(check_layer(L));
+  LUT_TRY(conv_dims(batch, cin, h, w, kh, kw, stride, pad));
+  if ((int64_t)L->c * L->v != (int64_t)cin * kh * kw) return fail(LUT_ERR_CONFIG, "patch cols != C*V");
+  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
+  const int64_t n = (int64_t)batch * ho * wo;
+  if (n == 0 || L->m == 0) return LUT_OK;
+  if (!x || !out || !codes_scratch) return fail(LUT_ERR_CONFIG, "null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t stride_c = lut_code_stride(L->c);
+  NvtxRange r_enc("lut.conv.encode");
+  LUT_TRY(encode_conv_strided(x, batch, cin, h, w, kh, kw, stride, pad, static_cast<const float*>(L->books_prep),
+                              L->c, L->k, L->v, codes_scratch, stride_c, near_tie_count, s));
+  r_enc.pop();
+  NvtxRange r_gat("lut.conv.gather");
+  if (L->onehot_image) {
+    const int digits = L->integer ? 1 : L->onehot_digits;
+    return onehot_gather(codes_scratch, stride_c, n, L->c, L->k, L->m, digits, L->onehot_image, L->scales,
+                         L->scale_mtile, L->bias, L->act, out, nullptr, (int64_t)ho * wo, s);
+  }
+  if (L->integer)
+    return gather_i8_strided(codes_scratch, 8, stride_c, n, L->c, L->k, L->m, L->q, L->scales, L->scale_mtile, L->bias,
+                             L->act, out, nullptr, (int64_t)ho * wo, nullptr, s, force_generic_env(), /*pdl=*/1);
+  return gather_f32_strided(codes_scratch, 8, stride_c, n, L->c, L->k, L->m, L->table, L->bias, L->act, out,
+                            (int64_t)ho * wo, nullptr, s, force_generic_env(), /*pdl=*/1);
 }
 
 // --------------------------------------------------------- host executor

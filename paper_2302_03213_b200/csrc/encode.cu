@@ -175,6 +175,7 @@ __device__ __forceinline__ void store_code_group(uint8_t* dst, uint32_t w0, uint
 template <int V, int kEncWarps, int kRPL, int CHAIN = 0>
 __global__ void __launch_bounds__((kEncWarps + 1) * 32, 1)
     encode_tma_kernel(const __grid_constant__ CUtensorMap tmap, const EncTmaParams p) {
+  grid_launch_dependents();  // a programmatic dependent (the gather) may start staging
   constexpr int kRowsPerPass = kEncWarps * 32;  // rows covered by one pass of all consumer lanes
   static_assert(kRowsPerPass * kRPL == kTileRows, "tile geometry");
   constexpr int NB = 32 / V;   // codebooks per 32-column box
@@ -430,6 +431,7 @@ template <int VT, class Rows>
 __global__ void __launch_bounds__(256) encode_rows_kernel(Rows rows, int64_t n, const float* __restrict__ prep,
                                                           int S, int C, int K, int V, uint8_t* __restrict__ codes,
                                                           int code_bits, int64_t code_stride, int* near_tie) {
+  grid_launch_dependents();  // a programmatic dependent (the gather) may start staging
   extern __shared__ float sh[];  // up to 2 prepared codebook records
   const int cpt = (code_bits == 4) ? 2 : 1;  // codebooks per thread (nibble pairs share a byte)
   const int c0 = blockIdx.y * cpt;
@@ -567,6 +569,7 @@ __device__ __forceinline__ void argmin_tree(const uint64_t (&acc)[KP], float& be
 
 template <int K, int KH>
 __global__ void __launch_bounds__(kConvWarps * 32, 1) encode_conv_plane_kernel(ConvPlaneParams p) {
+  grid_launch_dependents();  // a programmatic dependent (the gather) may start staging
   constexpr int V = KH * KH;
   constexpr int KP = K / 2;
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -910,16 +913,15 @@ int launch_conv_tc(const float* x, int batch, int cin, int h, int w, int stride,
                    const float* prep, int K, uint8_t* codes, int64_t code_stride, int* near_tie, cudaStream_t stream,
                    bool* used);
 
-int encode_conv(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad,
-                const float* prep, int C, int K, int V, uint8_t* codes, int code_bits, int* near_tie,
-                cudaStream_t stream) {
+int encode_conv_strided(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad,
+                        const float* prep, int C, int K, int V, uint8_t* codes, int64_t code_stride, int* near_tie,
+                        cudaStream_t stream) {
   const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
   const int64_t n = (int64_t)batch * ho * wo;
   if (n == 0 || C == 0) return LUT_OK;
   ConvRows rows{x, cin, h, w, kh, kw, stride, pad, ho, wo};
-  const int64_t code_stride = code_bits == 4 ? (C + 1) / 2 : C;
   const char* force = probe_env("LUTGPU_CONV_GENERIC");
-  if (code_bits == 8 && kh == 3 && kw == 3 && V == 9 && C == cin && !(force && atoi(force))) {
+  if (kh == 3 && kw == 3 && V == 9 && C == cin && !(force && atoi(force))) {
     bool used = false;
     int st = LUT_OK;
     const char* tc_env = probe_env("LUTGPU_CONV_TC");
@@ -939,7 +941,19 @@ int encode_conv(const float* x, int batch, int cin, int h, int w, int kh, int kw
     if (st != LUT_OK) return st;
     if (used) return LUT_OK;
   }
-  return launch_rows(nullptr, &rows, n, prep, C, K, V, codes, code_bits, code_stride, near_tie, stream);
+  return launch_rows(nullptr, &rows, n, prep, C, K, V, codes, 8, code_stride, near_tie, stream);
+}
+
+int encode_conv(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad,
+                const float* prep, int C, int K, int V, uint8_t* codes, int code_bits, int* near_tie,
+                cudaStream_t stream) {
+  if (code_bits == 8)
+    return encode_conv_strided(x, batch, cin, h, w, kh, kw, stride, pad, prep, C, K, V, codes, C, near_tie, stream);
+  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
+  const int64_t n = (int64_t)batch * ho * wo;
+  if (n == 0 || C == 0) return LUT_OK;
+  ConvRows rows{x, cin, h, w, kh, kw, stride, pad, ho, wo};
+  return launch_rows(nullptr, &rows, n, prep, C, K, V, codes, code_bits, (C + 1) / 2, near_tie, stream);
 }
 
 int im2col(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad, float* cols,

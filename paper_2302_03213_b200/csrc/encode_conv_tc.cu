@@ -150,6 +150,7 @@ __device__ __forceinline__ int conv_screen(const uint32_t (&dv)[16], const float
 }
 
 __global__ void __launch_bounds__(kCtThreads, 1) encode_conv_tc_kernel(const ConvTcParams p) {
+  grid_launch_dependents();  // a programmatic dependent (the gather) may start staging
   constexpr int V = 9, K = 16;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);

@@ -114,6 +114,7 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 template <int GR, int NK>
 __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
     encode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const EncTcParams p) {
+  grid_launch_dependents();  // a programmatic dependent (the gather) may start staging
   constexpr int kTcStages = TcGeom<GR, NK>::stages;
   constexpr int kTcStageBytes = tc_stage_bytes<NK>();
   constexpr int kAux = 16384 + NK * 128;             // aux offset inside a stage

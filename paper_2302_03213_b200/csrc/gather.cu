@@ -36,6 +36,7 @@ struct GatherArgs {
   // i8
   const float* scales;
   int scale_mtile;
+  int pdl;  // launched as a programmatic dependent of the encode (lut_layer_forward)
 };
 
 // Row base and column stride of the output: row-major (N, M) or NCHW (one 32-bit
@@ -348,6 +349,7 @@ __global__ void __launch_bounds__(T, T <= 128 ? 4 : 1)
       __syncthreads();
       stage_f32_slice<NP, T>(tsm, table, g.M, C, K, m0);
       __syncthreads();
+      if (cur < 0) grid_dependency_wait();  // the table slice is staged while the encode finishes
       cur = mt;
     }
     const int64_t row = rb * T + threadIdx.x;
@@ -462,6 +464,7 @@ __global__ void __launch_bounds__(T, T <= 128 ? 4 : 1)
       __syncthreads();
       stage_i8_slice<NO, T>(qsm, q8, g.M, C, K, m0);
       __syncthreads();
+      if (cur < 0) grid_dependency_wait();
       cur = mt;
     }
     const int64_t row = rb * T + threadIdx.x;
@@ -581,6 +584,7 @@ static GatherArgs make_args(const uint8_t* codes, int code_bits, int64_t n, int 
   g.err = err;
   g.scales = nullptr;
   g.scale_mtile = 0;
+  g.pdl = 0;
   return g;
 }
 
@@ -610,6 +614,23 @@ static int launch_rows(void (*kern)(GatherArgs, const T*, int64_t), int nmt, siz
   if (band_rb > max_band) band_rb = max_band;
   if (band_rb < 1) band_rb = 1;
   if (band_rb > nrb) band_rb = nrb;
+  if (g.pdl) {
+    // programmatic dependent launch: CTAs start on the SMs the encode leaves free
+    // and stage their table slices before griddepcontrol.wait (the codes)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(TH);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, g, table, band_rb);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernelEx(gather, PDL)");
+    return LUT_OK;
+  }
   kern<<<grid, TH, smem, stream>>>(g, table, band_rb);
   return LUT_OK;
 }
@@ -625,10 +646,11 @@ static int launch_f32(int nmt, size_t smem, const GatherArgs& g, const float* ta
 
 int gather_f32_strided(const uint8_t* codes, int code_bits, int64_t code_stride, int64_t n, int C, int K, int M,
                        const float* table, const float* bias, int act, float* out, int64_t out_hw, int* err,
-                       cudaStream_t stream, int force_generic) {
+                       cudaStream_t stream, int force_generic, int pdl) {
   if (n == 0 || M == 0) return LUT_OK;
   GatherArgs g = make_args(codes, code_bits, n, C, K, M, bias, act, out, nullptr, out_hw, err);
   g.code_stride = code_stride;
+  g.pdl = pdl;
   const size_t budget = 200 * 1024;
   const size_t per_chunk = (size_t)C * K * 8;  // SMEM bytes per 2-column chunk
   int NP = 0;
@@ -674,10 +696,11 @@ static int launch_i8(int nmt, size_t smem, const GatherArgs& g, const int8_t* q,
 
 int gather_i8_strided(const uint8_t* codes, int code_bits, int64_t code_stride, int64_t n, int C, int K, int M,
                       const int8_t* q, const float* scales, int scale_mtile, const float* bias, int act, float* out,
-                      int32_t* out_i32, int64_t out_hw, int* err, cudaStream_t stream, int force_generic) {
+                      int32_t* out_i32, int64_t out_hw, int* err, cudaStream_t stream, int force_generic, int pdl) {
   if (n == 0 || M == 0) return LUT_OK;
   GatherArgs g = make_args(codes, code_bits, n, C, K, M, bias, act, out, out_i32, out_hw, err);
   g.code_stride = code_stride;
+  g.pdl = pdl;
   g.scales = scales;
   g.scale_mtile = scale_mtile;
   const size_t budget = 200 * 1024;
@@ -727,14 +750,14 @@ int gather_f32(const uint8_t* codes, int code_bits, int64_t n, int C, int K, int
                const float* bias, int act, float* out, int64_t out_hw, int* err, cudaStream_t stream,
                int force_generic) {
   return gather_f32_strided(codes, code_bits, code_bits == 4 ? (C + 1) / 2 : C, n, C, K, M, table, bias, act, out,
-                            out_hw, err, stream, force_generic);
+                            out_hw, err, stream, force_generic, 0);
 }
 
 int gather_i8(const uint8_t* codes, int code_bits, int64_t n, int C, int K, int M, const int8_t* q,
               const float* scales, int scale_mtile, const float* bias, int act, float* out, int32_t* out_i32,
               int64_t out_hw, int* err, cudaStream_t stream, int force_generic) {
   return gather_i8_strided(codes, code_bits, code_bits == 4 ? (C + 1) / 2 : C, n, C, K, M, q, scales, scale_mtile,
-                           bias, act, out, out_i32, out_hw, err, stream, force_generic);
+                           bias, act, out, out_i32, out_hw, err, stream, force_generic, 0);
 }
 
 }  // namespace lutgpu

@@ -11,6 +11,8 @@ device-resident pipelines (LutLinear applies over the last dim).
 
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 import torch
 
@@ -72,33 +74,13 @@ def conv_forward(x, lut: LutLayer, cin: int, kernel: int, stride: int, pad: int,
     dev = lut.device
     x_dev = D.to_device(x, F32, dev)
     n = b * ho * wo
-    codes = torch.empty((n, max(lut.c, 1)), dtype=torch.uint8, device=dev)
-    near = torch.zeros(1, dtype=torch.int32, device=dev)
-    lib = load()
-    check(lib.lut_encode_conv_f32(D.ptr(x_dev), b, cin, h, w, kernel, kernel, stride, pad, D.ptr(lut.books_prep),
-                                  lut.c, lut.k, lut.v, D.ptr(codes), 8, D.ptr(near), D.stream_ptr()), "LutConv")
+    codes = torch.empty((n, lut.code_stride), dtype=torch.uint8, device=dev)
     out = torch.empty((b, lut.m, ho, wo), dtype=torch.float32, device=dev)
-    act = ACTS[lut.act]
-    if lut.uses_tensor_cores(bool(integer)):
-        # the one-hot gather TMA-loads 16-byte code rows: pad the (n, C) codes
-        stride_c = lut.code_stride
-        padded = torch.zeros((n, stride_c), dtype=torch.uint8, device=dev)
-        padded[:, :lut.c] = codes
-        desc = lut.desc(bool(integer))
-        check(lib.lut_gather_onehot(D.ptr(padded), stride_c, n, lut.c, lut.k, lut.m, desc.onehot_digits,
-                                    desc.onehot_image, desc.scales if integer else None,
-                                    lut.qtable.scale_mtile if integer else 0, D.ptr(lut.bias), act, D.ptr(out),
-                                    None, ho * wo, D.stream_ptr()), "LutConv")
-    else:
-        # codes come from the distance encoder, so they are < K by construction: no
-        # error flag (and no stream sync: the layer stays capturable in a CUDA graph)
-        if integer and lut.per_codebook_scales:
-            _gather_f32(codes, lut.dequantized(), lut.bias, act, lut.c, lut.k, lut.m, None, out_hw=ho * wo, out=out)
-        elif integer:
-            _gather_i8_f32(codes, lut.qtable.q, lut.qtable.scales_tensor(dev), lut.qtable.scale_mtile, lut.bias,
-                           act, lut.c, lut.k, lut.m, None, out_hw=ho * wo, out=out)
-        else:
-            _gather_f32(codes, lut.table, lut.bias, act, lut.c, lut.k, lut.m, None, out_hw=ho * wo, out=out)
+    # one ABI call: fused-im2col encode, then the lookup (launched as a programmatic
+    # dependent of the encode) storing NCHW; codes come from the distance encoder,
+    # so they are < K by construction and no error flag / stream sync is needed
+    check(load().lut_conv_layer_forward(C.byref(lut.desc(bool(integer))), D.ptr(x_dev), b, cin, h, w, kernel, kernel,
+                                        stride, pad, D.ptr(out), D.ptr(codes), None, D.stream_ptr()), "LutConv")
     return D.from_device(out, kind)
 
 
