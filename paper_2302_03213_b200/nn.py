@@ -19,7 +19,7 @@ import torch
 from . import _device as D
 from ._lib import check, load
 from .errors import ConfigError, ShapeError
-from .kernels import ACTS, EncodeStats, KernelPlan, _gather_f32, _gather_i8_f32, lut_layer_infer
+from .kernels import KernelPlan, lut_layer_infer
 from .layer import LutLayer, as_device_layer
 from .tensor import conv_out_hw
 

@@ -61,3 +61,16 @@ def test_cmtile_layer_and_ffn(L):
     ffn, x = W.ffn_pair(torch.device("cuda", 0), tokens=512, scale_mtile=128, per_codebook=True)
     y = ffn(x)
     assert y.shape == (512, 768) and torch.isfinite(y).all()
+
+
+def test_cmtile_not_storable_in_lutn(L):
+    """The version-1 .lutn container holds one scale per table (container.py):
+    per-(codebook, m-tile) scales are refused with ContainerError, not dropped."""
+    rng = O.make_rng(5)
+    books = rng.standard_normal((4, 16, 8)).astype(F32)
+    w = rng.standard_normal((32, 64)).astype(F32)
+    layer = L.LutLayer(cfg=L.PqConfig(v=8, k=16), books=books, weight=w, qat=True, scale_mtile=32,
+                       scale_per_codebook=True)
+    dense = L.LutDense(layer)
+    with pytest.raises(L.ContainerError):
+        L.model_bytes(L.Model([dense]))
