@@ -38,7 +38,8 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--table", choices=["f32", "i8"], default="i8")
+    p.add_argument("--table", choices=["f32", "i8"], default=None,
+                   help="table kind (default: BASELINE's — int8 for cfg2/cfg4/cfg5, fp32 for cfg1/cfg3)")
     p.add_argument("--k", type=int, default=16)
     p.add_argument("--rows", type=int, default=1 << 20, help="rows per GPU")
     p.add_argument("--dim", type=int, default=4096)
@@ -344,6 +345,8 @@ class _Null:
 
 def main():
     args = parse()
+    if args.table is None:
+        args.table = "f32" if args.workload in ("cfg1", "cfg3") else "i8"
     if args.workload != "cfg5":
         return main_stack(args)
     rank = int(os.environ.get("RANK", "0"))
@@ -532,6 +535,55 @@ def main():
 # ------------------------------------------------------------- configs 1-4
 
 
+def _host(t):
+    return t.detach().cpu().numpy() if hasattr(t, "detach") else np.asarray(t)
+
+
+def stack_cpu_baseline(wl, objs, unit_rows):
+    """The reference's CPU algorithm (oracle port: f64 encode, ascending-c f32 /
+    exact int8 lookups, the same epilogues) on the same layers, one host thread
+    (the reference's contract), on a bounded sample of the step's rows."""
+    from oracle import lut_oracle as O
+
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    t0 = time.perf_counter()
+    if wl == "cfg1":
+        layer, x = objs
+        a = _host(x)
+        O.lut_layer_infer(a, _host(layer.books), table=_host(layer.table), integer=False)
+        rows, sample = a.shape[0], f"all {a.shape[0]} rows"
+    elif wl == "cfg2":
+        ffn, x, mt, per_cb = objs
+        a = _host(x[:256])
+        h = a
+        for lin in (ffn.up, ffn.down):
+            lut = lin.lut
+            enc = O.centroid_search_fast(h, _host(lut.books))
+            q, sc = _host(lut.qtable.q), _host(lut.qtable.scales_tensor(lut.device))
+            if per_cb:
+                y = O.lut_gather_accumulate_cmtile(enc, q, sc.reshape(lut.c, -1), mt)
+            elif mt:
+                y = O.lut_gather_accumulate_mtile(enc, q, sc, mt)
+            else:
+                y = O.lut_gather_accumulate(enc, q, sc[0])
+            h = O.gelu_erf(y) if lut.act == "gelu" else y
+        rows, sample = a.shape[0], "256 of 4096 tokens"
+    elif wl == "cfg3":
+        convs = objs
+        rows = 0
+        for conv, x in convs:
+            xs = _host(x[:2])
+            cols = O.im2col(xs, 3, 3, 1, 1)
+            lut = conv.lut
+            O.lut_matmul_ref(O.centroid_search_fast(cols, _host(lut.books)), _host(lut.table))
+            rows += cols.shape[0]
+        sample = "2 of 256 images per stage"
+    else:
+        return None
+    dt = time.perf_counter() - t0
+    return {"value": rows / dt, "unit": f"{unit_rows}/s", "cores": 1, "kind": "port", "sample": sample}
+
+
 STACKS = {
     "cfg1": "BASELINE configs[0]: single LUT Linear N=1024, 768->768, V=16, K=16",
     "cfg2": "BASELINE configs[1]: BERT-base FFN pair 4096 tokens, 768->3072 (GELU) ->768, V=32, K=16, int8",
@@ -568,11 +620,13 @@ def main_stack(args):
         layer, x = W.linear(dev, 1024, 768, 768, 16, 16, integer, gather="auto")
         mod = LutLinear(layer, integer)
         fn, rows, unit_rows = (lambda: mod(x)), 1024, "rows"
+        cpu_objs = (layer, x) if not integer else None
     elif wl == "cfg2":
         # BASELINE configs[1]: int8 tables with a per-(c, m-tile) fp32 scale
         mt = 128 if args.scale_mtile < 0 else args.scale_mtile
         ffn, x = W.ffn_pair(dev, tokens=4096, scale_mtile=mt, per_codebook=not args.per_table_scales)
         fn, rows, unit_rows = (lambda: ffn(x)), 4096, "tokens"
+        cpu_objs = (ffn, x, mt, not args.per_table_scales)
     elif wl == "cfg3":
         convs = W.resnet_convs(dev, batch=256)
         x = convs[0][1]
@@ -583,9 +637,11 @@ def main_stack(args):
 
         rows = sum(xx.shape[0] * xx.shape[2] * xx.shape[3] for _, xx in convs)
         unit_rows = "output pixels"
+        cpu_objs = convs
     else:
         model, x = W.bert_encoder(dev, batch=64, seq=128, scale_mtile=max(0, args.scale_mtile))
         fn, rows, unit_rows = (lambda: model(x)), 64 * 128, "tokens"
+        cpu_objs = None
 
     # per-LUT-layer events + algorithmic HBM bytes (fused layer formula)
     luts = []
@@ -686,6 +742,9 @@ def main_stack(args):
     e2e_s = statistics.median(times)
     hbm_peak, _, peak_kind = peaks()
     achieved = lut_bytes / (lut_ms / 1e3) / 1e9
+    cpu = None
+    if rank == 0 and cpu_objs is not None and not args.no_cpu:
+        cpu = stack_cpu_baseline(wl, cpu_objs, unit_rows)
     if world > 1:
         dist.destroy_process_group()
     if rank != 0:
@@ -693,12 +752,12 @@ def main_stack(args):
     line = {"metric": METRIC, "value": rows * world / (ms / 1e3), "unit": f"{unit_rows}/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32" if wl in ("cfg1", "cfg3") and not integer else "f32-encode/int8-table/int32-acc",
+            "dtype": "f32" if not integer else "f32-encode/int8-table/int32-acc",
             "data": "synthetic (seeded torch.randn on device; random-init weights; centroids sampled from a "
                     "held-out batch)",
             "config": {"workload": STACKS[wl], "rows_per_step": rows, "cuda_graph": graph is not None,
                        "l2": "256 MB buffer written, then a 256 MB buffer read, between timed steps",
-                       "scale_mtile": args.scale_mtile,
+                       "scale_mtile": args.scale_mtile, "table": args.table,
                        **({"int8_scales": "per (m-tile)" if args.per_table_scales else "per (codebook, m-tile)"}
                           if wl == "cfg2" else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -708,7 +767,7 @@ def main_stack(args):
             "clocks": clocks.summary(), "gpu_launches": None,
             "e2e": {"value": rows * world / e2e_s, "unit": f"{unit_rows}/s", "h2d_bytes_per_step": x.numel() * 4,
                     "d2h_bytes_per_step": y0.numel() * 4},
-            "cpu_baseline": None}
+            "cpu_baseline": cpu}
     print(json.dumps(line), flush=True)
 
 

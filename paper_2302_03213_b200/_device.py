@@ -41,13 +41,10 @@ def to_device(x, np_dtype, device: torch.device | None = None) -> torch.Tensor:
         t = x.to(device=device, dtype=tdt, non_blocking=True)
         return t.contiguous()
     arr = np.ascontiguousarray(x, dtype=np_dtype)
-    t = torch.from_numpy(arr)
-    if arr.size * arr.itemsize >= (1 << 20):
-        try:
-            t = t.pin_memory()
-        except RuntimeError:
-            pass
-    return t.to(device, non_blocking=False)
+    # a plain pageable copy: pinning a fresh host buffer per call (cudaHostAlloc +
+    # a host memcpy) costs more than it saves for a one-shot transfer; large
+    # numpy layer inputs stream through the native executor's pinned chunks
+    return torch.from_numpy(arr).to(device, non_blocking=False)
 
 
 def from_device(t: torch.Tensor, kind: str):

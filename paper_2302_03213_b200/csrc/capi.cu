@@ -66,6 +66,7 @@ int gather_i8_strided(const uint8_t* codes, int code_bits, int64_t code_stride, 
                       int32_t* out_i32, int64_t out_hw, int* err, cudaStream_t stream, int force_generic, int pdl = 0);
 int build_table(const float* b, int M, const float* books, int C, int K, int V, float* table,
                 cudaStream_t stream);
+
 size_t quantize_scratch_bytes(int C, int K, int M, int mtile);
 int matmul_ref(const float* a, const float* b, int64_t n, int d, int m, float* out, cudaStream_t stream);
 int quantize_table(const float* t, int C, int K, int M, int mtile, int8_t* q, float* scales, void* scratch,

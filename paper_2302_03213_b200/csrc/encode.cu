@@ -30,6 +30,7 @@
 #include <float.h>
 
 #include "common.cuh"
+#include "encode_dev.cuh"
 
 namespace lutgpu {
 
@@ -101,26 +102,6 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   return d;
 }
 
-__device__ __forceinline__ float tau_coef(int v) { return (4.0f * v + 16.0f) * 5.9604645e-8f; }
-
-// Literal f64 re-decision (encode_hard semantics) for one (row, codebook).
-template <class GetA>
-__device__ __noinline__ int exact_argmin(GetA get_a, const float* __restrict__ cent, int K, int V) {
-  double best = 0.0;
-  int bi = 0;
-  for (int k = 0; k < K; ++k) {
-    double s = 0.0;
-    for (int j = 0; j < V; ++j) {
-      double diff = (double)get_a(j) - (double)cent[k * V + j];
-      s = __dadd_rn(s, __dmul_rn(diff, diff));
-    }
-    if (k == 0 || s < best) {
-      best = s;
-      bi = k;
-    }
-  }
-  return bi;
-}
 
 // --------------------------------------------------------------- TMA path
 

@@ -324,6 +324,83 @@ __device__ __forceinline__ void stage_i8_slice(uint2* qsm, const int8_t* __restr
   }
 }
 
+// One unit of the row-parallel f32 gather: T rows (thread = row) x 2*NP columns
+// starting at m0, the m-tile's table slice staged at sbase ([c][chunk][k] pairs).
+template <int NP, int T>
+__device__ __forceinline__ void f32_rows_unit(const GatherArgs& g, uint32_t sbase, int m0, int64_t rb, bool v16,
+                                              int pow2, bool& bad) {
+  const int K = g.K, C = g.C;
+  const uint32_t cstep = (uint32_t)(NP * K * 8);  // bytes per codebook
+  const int64_t row = rb * T + threadIdx.x;
+  const bool live = row < g.n;
+  const int64_t rr = live ? row : g.n - 1;
+  uint64_t acc[NP];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) acc[j] = 0ull;  // (+0.0f, +0.0f)
+  if (g.code_bits == 8) {
+    RowCodes rc{g.codes + rr * g.code_stride, v16};
+    int c0 = 0;
+    // the next 16 codes are loaded while the current 16 are looked up (a
+    // load-then-use loop serialises one global latency per 16 codebooks)
+    uint4 wn = C >= 16 ? rc.load16(0) : make_uint4(0u, 0u, 0u, 0u);
+    for (; c0 + 16 <= C; c0 += 16) {
+      const uint4 w = wn;
+      if (c0 + 32 <= C) wn = rc.load16(c0 + 16);
+      bad |= codes_bad(w, K, pow2);
+#pragma unroll
+      for (int s = 0; s < 16; ++s) {
+        uint32_t code = code_byte(w, s);
+        code = pow2 ? (code & (uint32_t)(K - 1)) : min(code, (uint32_t)(K - 1));
+        const uint32_t a = sbase + (uint32_t)(c0 + s) * cstep + code * 8u;
+#pragma unroll
+        for (int j = 0; j < NP; ++j) fadd2(acc[j], lds64(a + (uint32_t)(j * K * 8)));
+      }
+    }
+    for (; c0 < C; ++c0) {
+      uint32_t code = __ldg(rc.p + c0);
+      bad |= code >= (uint32_t)K;
+      code = min(code, (uint32_t)(K - 1));
+      const uint32_t a = sbase + (uint32_t)c0 * cstep + code * 8u;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) fadd2(acc[j], lds64(a + (uint32_t)(j * K * 8)));
+    }
+  } else {
+    for (int c = 0; c < C; ++c) {
+      uint32_t code = (uint32_t)read_code(g, rr, c);
+      bad |= code >= (uint32_t)K;
+      code = min(code, (uint32_t)(K - 1));
+      const uint32_t a = sbase + (uint32_t)c * cstep + code * 8u;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) fadd2(acc[j], lds64(a + (uint32_t)(j * K * 8)));
+    }
+  }
+  if (!live) return;
+  int64_t obase, ocs;
+  out_row(g, row, obase, ocs);
+  const bool vrow = ocs == 1 && (g.M & 3) == 0 && (reinterpret_cast<uintptr_t>(g.out) & 15) == 0;
+#pragma unroll
+  for (int j = 0; j < NP; j += 2) {
+    float v[4];
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v[0]), "=f"(v[1]) : "l"(acc[j]));
+    if (j + 1 < NP) {
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(v[2]), "=f"(v[3]) : "l"(acc[j + 1]));
+    } else {
+      v[2] = v[3] = 0.f;
+    }
+    const int col = m0 + 2 * j;
+    const int ncol = j + 1 < NP ? 4 : 2;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = (e < ncol && col + e < g.M) ? f32_epilogue(g, v[e], col + e) : 0.f;
+    if (vrow && ncol == 4 && col + 3 < g.M) {
+      *reinterpret_cast<float4*>(g.out + obase + col) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e < ncol && col + e < g.M) g.out[obase + (int64_t)(col + e) * ocs] = v[e];
+    }
+  }
+}
+
 // Thread block of T threads; NP chunks of 2 f32 columns per thread (MT = 2 * NP).
 template <int NP, int T>
 __global__ void __launch_bounds__(T, T <= 128 ? 4 : 1)
@@ -336,7 +413,6 @@ __global__ void __launch_bounds__(T, T <= 128 ? 4 : 1)
   const int pow2 = (K & (K - 1)) == 0;
   const bool v16 = g.code_bits == 8 && (g.code_stride & 15) == 0 && (reinterpret_cast<uintptr_t>(g.codes) & 15) == 0;
   const uint32_t sbase = smem_u32(tsm);
-  const uint32_t cstep = (uint32_t)(NP * K * 8);  // bytes per codebook
   RowWalk walk;
   walk.init(nrb, nmt, band_rb);
   int cur = -1;
@@ -352,74 +428,7 @@ __global__ void __launch_bounds__(T, T <= 128 ? 4 : 1)
       if (cur < 0) grid_dependency_wait();  // the table slice is staged while the encode finishes
       cur = mt;
     }
-    const int64_t row = rb * T + threadIdx.x;
-    const bool live = row < g.n;
-    const int64_t rr = live ? row : g.n - 1;
-    uint64_t acc[NP];
-#pragma unroll
-    for (int j = 0; j < NP; ++j) acc[j] = 0ull;  // (+0.0f, +0.0f)
-    if (g.code_bits == 8) {
-      RowCodes rc{g.codes + rr * g.code_stride, v16};
-      int c0 = 0;
-      // the next 16 codes are loaded while the current 16 are looked up (a
-      // load-then-use loop serialises one global latency per 16 codebooks)
-      uint4 wn = C >= 16 ? rc.load16(0) : make_uint4(0u, 0u, 0u, 0u);
-      for (; c0 + 16 <= C; c0 += 16) {
-        const uint4 w = wn;
-        if (c0 + 32 <= C) wn = rc.load16(c0 + 16);
-        bad |= codes_bad(w, K, pow2);
-#pragma unroll
-        for (int s = 0; s < 16; ++s) {
-          uint32_t code = code_byte(w, s);
-          code = pow2 ? (code & (uint32_t)(K - 1)) : min(code, (uint32_t)(K - 1));
-          const uint32_t a = sbase + (uint32_t)(c0 + s) * cstep + code * 8u;
-#pragma unroll
-          for (int j = 0; j < NP; ++j) fadd2(acc[j], lds64(a + (uint32_t)(j * K * 8)));
-        }
-      }
-      for (; c0 < C; ++c0) {
-        uint32_t code = __ldg(rc.p + c0);
-        bad |= code >= (uint32_t)K;
-        code = min(code, (uint32_t)(K - 1));
-        const uint32_t a = sbase + (uint32_t)c0 * cstep + code * 8u;
-#pragma unroll
-        for (int j = 0; j < NP; ++j) fadd2(acc[j], lds64(a + (uint32_t)(j * K * 8)));
-      }
-    } else {
-      for (int c = 0; c < C; ++c) {
-        uint32_t code = (uint32_t)read_code(g, rr, c);
-        bad |= code >= (uint32_t)K;
-        code = min(code, (uint32_t)(K - 1));
-        const uint32_t a = sbase + (uint32_t)c * cstep + code * 8u;
-#pragma unroll
-        for (int j = 0; j < NP; ++j) fadd2(acc[j], lds64(a + (uint32_t)(j * K * 8)));
-      }
-    }
-    if (!live) continue;
-    int64_t obase, ocs;
-    out_row(g, row, obase, ocs);
-    const bool vrow = ocs == 1 && (g.M & 3) == 0 && (reinterpret_cast<uintptr_t>(g.out) & 15) == 0;
-#pragma unroll
-    for (int j = 0; j < NP; j += 2) {
-      float v[4];
-      asm("mov.b64 {%0, %1}, %2;" : "=f"(v[0]), "=f"(v[1]) : "l"(acc[j]));
-      if (j + 1 < NP) {
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(v[2]), "=f"(v[3]) : "l"(acc[j + 1]));
-      } else {
-        v[2] = v[3] = 0.f;
-      }
-      const int col = m0 + 2 * j;
-      const int ncol = j + 1 < NP ? 4 : 2;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = (e < ncol && col + e < g.M) ? f32_epilogue(g, v[e], col + e) : 0.f;
-      if (vrow && ncol == 4 && col + 3 < g.M) {
-        *reinterpret_cast<float4*>(g.out + obase + col) = make_float4(v[0], v[1], v[2], v[3]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (e < ncol && col + e < g.M) g.out[obase + (int64_t)(col + e) * ocs] = v[e];
-      }
-    }
+    f32_rows_unit<NP, T>(g, sbase, m0, rb, v16, pow2, bad);
   }
   if (bad && g.err) atomicMax(g.err, (int)LUT_ERR_CORRUPTION);
 }

@@ -206,3 +206,25 @@ def test_bench_kernel_report(L):
         L.bench_kernel((8, 10, 4, 4, 3))
     with pytest.raises(L.ConfigError):
         L.bench_kernel((8, 8, 4, 4, 2), repetitions=3)
+
+
+@pytest.mark.parametrize("n,c,k,v,m", [(1024, 48, 16, 16, 768), (300, 7, 8, 4, 33), (5000, 24, 16, 32, 130),
+                                       (1, 3, 16, 9, 5), (16384, 16, 16, 8, 64)])
+def test_small_layer_bitwise(L, n, c, k, v, m):
+    """Few-row fp32 layers (configs[0] and smaller / ragged shapes) through
+    lut_layer_forward: bytes equal to the oracle's lut_layer_infer
+    (kernels.py:143-178), bias and ReLU epilogue included."""
+    import torch
+
+    rng = O.make_rng(n + c)
+    books = rng.standard_normal((c, k, v)).astype(F32)
+    w = (rng.standard_normal((c * v, m)) / np.sqrt(c * v)).astype(F32)
+    bias = rng.standard_normal(m).astype(F32)
+    a = rng.standard_normal((n, c * v)).astype(F32)
+    layer = L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=books, weight=w, bias=bias)
+    table = O.build_table(w, books)
+    want = O.lut_layer_infer(a, books, table=table, bias=bias, integer=False)
+    got = layer.forward_device(torch.from_numpy(a).cuda(), False).cpu().numpy()
+    assert got.tobytes() == want.tobytes()
+    relu = layer.with_act("relu").forward_device(torch.from_numpy(a).cuda(), False).cpu().numpy()
+    assert relu.tobytes() == np.maximum(want, 0).astype(F32).tobytes()
