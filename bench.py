@@ -80,14 +80,18 @@ def peaks():
 _CPU_WORK = None  # set before the fork pool starts; workers inherit it (no pickling in the timed loop)
 
 
+_CPU_PLAN = (64, 8)  # KernelPlan(n_block, k_block) of the encode (kernels.py:39-59 default)
+
+
 def _cpu_worker(rows):
     from oracle import lut_oracle as O
 
     a, books, table, q, scale, integer = _CPU_WORK
     a = a[:rows]
+    nb, kb = _CPU_PLAN
     if integer:
-        return O.lut_layer_infer(a, books, q=q, scale=scale).shape[0]
-    return O.lut_layer_infer(a, books, table=table, integer=False).shape[0]
+        return O.lut_layer_infer(a, books, q=q, scale=scale, n_block=nb, k_block=kb).shape[0]
+    return O.lut_layer_infer(a, books, table=table, integer=False, n_block=nb, k_block=kb).shape[0]
 
 
 def _cpu_pool_time(rows_per_core, workers, steps, warmup, ctx):
@@ -144,6 +148,13 @@ def cpu_reference(dim, m, v, k, integer, rows_per_core, steps, warmup, seed=7, e
                             "linear": abs(res["value"] / r_half - 1.0) < 0.15}
         med_1, _ = _cpu_pool_time(half, 1, 1, 0, ctx)
         res["one_core"] = {"value": half / med_1, "unit": UNIT, "cores": 1, "rows_sampled": half}
+        # the large-block plan SURVEY §8(d) asks for: KernelPlan(n_block=8192, k_block=16)
+        global _CPU_PLAN
+        _CPU_PLAN = (8192, 16)
+        med_p, _ = _cpu_pool_time(half, cores, 1, 0, ctx)
+        _CPU_PLAN = (64, 8)
+        res["plan_8192_16"] = {"value": half * cores / med_p, "unit": UNIT, "cores": cores,
+                               "rows_sampled": half * cores, "plan": "KernelPlan(n_block=8192, k_block=16)"}
     return res
 
 
@@ -374,6 +385,7 @@ def main():
                 "data": "synthetic", "config": config, "effective_gops": eff,
                 "cpu_baseline": {k_: ref[k_] for k_ in ("value", "unit", "cores", "kind", "sample")},
                 "one_core": ref.get("one_core"), "linearity": ref.get("linearity"),
+                "plan_8192_16": ref.get("plan_8192_16"),
                 "e2e": {"value": ref["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -529,6 +541,7 @@ def main():
         line["cpu_baseline"] = {k_: cpu[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
         line["cpu_baseline"]["one_core"] = cpu.get("one_core")
         line["cpu_baseline"]["linearity"] = cpu.get("linearity")
+        line["cpu_baseline"]["plan_8192_16"] = cpu.get("plan_8192_16")
     print(json.dumps(line), flush=True)
 
 
@@ -673,12 +686,30 @@ def main_stack(args):
     fn()
     torch.cuda.synchronize()
     lut_ms, lut_bytes = 0.0, 0
+    # SURVEY §8(d) bound per LUT layer: max(HBM bytes / HBM peak, lookup bytes /
+    # SMEM (CUDA-core gathers) or sparse-MMA time (tensor gathers), encode FMAs /
+    # FP32 rate); the step's bound is their sum over the layers
+    hbm_peak_bps = peaks()[0] * 1e9
+    clk = 1.965e9
+    t_bound = 0.0
+    bound_terms = {"hbm": 0.0, "smem_or_mma": 0.0, "ffma": 0.0}
     for m_, a, e0, y, e1 in marks:
         lut = m_.lut
         intg = getattr(m_, "integer", None)
-        s_ = 1 if (lut.has_qtable if intg is None else intg) else 4
+        intg = lut.has_qtable if intg is None else bool(intg)
+        s_ = 1 if intg else 4
         lut_ms += e0.elapsed_time(e1)
-        lut_bytes += 4 * a.numel() + s_ * lut.c * lut.k * lut.m + 4 * lut.c * lut.k * lut.v + 4 * y.numel()
+        hbm_b = 4 * a.numel() + s_ * lut.c * lut.k * lut.m + 4 * lut.c * lut.k * lut.v + 4 * y.numel()
+        lut_bytes += hbm_b
+        nrows = y.numel() // lut.m
+        if lut.uses_tensor_cores(intg):
+            gather_t = nrows * lut.m * lut.c * lut.k * (1 if intg else lut.f32_digits) / (16384 * 148 * clk)
+        else:
+            gather_t = nrows * lut.m * lut.c * s_ / (148 * 128 * clk)
+        terms = {"hbm": hbm_b / hbm_peak_bps, "smem_or_mma": gather_t,
+                 "ffma": nrows * lut.c * lut.v * lut.k / (148 * 128 * clk)}
+        t_bound += max(terms.values())
+        bound_terms[max(terms, key=terms.get)] += max(terms.values())
     for hk in hooks:
         hk.remove()
 
@@ -763,7 +794,11 @@ def main_stack(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": None, "kernel": "LUT layers (encode+gather)",
                          "peak_kind": peak_kind, "algorithmic_bytes": lut_bytes, "lut_ms_eager": lut_ms,
-                         "lut_layers": len(marks)},
+                         "lut_layers": len(marks),
+                         "survey_bound": {"t_bound_ms": t_bound * 1e3,
+                                          "binding": max(bound_terms, key=bound_terms.get),
+                                          "terms_ms": {k_: v_ * 1e3 for k_, v_ in bound_terms.items()},
+                                          "frac_of_step": t_bound * 1e3 / ms}},
             "clocks": clocks.summary(), "gpu_launches": None,
             "e2e": {"value": rows * world / e2e_s, "unit": f"{unit_rows}/s", "h2d_bytes_per_step": x.numel() * 4,
                     "d2h_bytes_per_step": y0.numel() * 4},

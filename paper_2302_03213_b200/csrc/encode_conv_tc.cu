@@ -273,6 +273,16 @@ __global__ void __launch_bounds__(kCtThreads, 1) encode_conv_tc_kernel(const Con
       const int oy = pix / p.wo, ox = pix - oy * p.wo;
       const int y0 = oy * p.stride - p.pad, x0 = ox * p.stride - p.pad;
       const float* img = pl + (size_t)bl * kCtCh * plane;
+      // the patch's 9 plane offsets and padding mask are the same for every channel
+      int poff[V];
+      uint32_t pmask = 0u;
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const int iy = y0 + j / 3, ix = x0 + j % 3;
+        const bool in = (unsigned)iy < (unsigned)p.h && (unsigned)ix < (unsigned)p.w;
+        poff[j] = in ? iy * p.w + ix : 0;
+        pmask |= in ? (1u << j) : 0u;
+      }
       uint64_t codes_lo = 0ull, codes_hi = 0ull;  // this pixel's 16 codes, byte c at 8 * c
       // 2-slot TMEM ring per group (A_hi 16 | A_lo 16 | D 16 columns): the screen of
       // channel c - 1 runs while channel c's MMAs execute.
@@ -284,14 +294,11 @@ __global__ void __launch_bounds__(kCtThreads, 1) encode_conv_tc_kernel(const Con
         if (cl < nch) {
           const float* pc = img + (size_t)cl * plane;
 #pragma unroll
-          for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-            for (int dx = 0; dx < 3; ++dx) {
-              const int iy = y0 + dy, ix = x0 + dx;
-              const float v = ((unsigned)iy < (unsigned)p.h && (unsigned)ix < (unsigned)p.w) ? pc[iy * p.w + ix] : 0.0f;
-              a[dy * 3 + dx] = v;
-              asq = fmaf(v, v, asq);
-            }
+          for (int j = 0; j < V; ++j) {
+            const float v = ((pmask >> j) & 1u) ? pc[poff[j]] : 0.0f;
+            a[j] = v;
+            asq = fmaf(v, v, asq);
+          }
           // 3xTF32: a = a_hi + a_lo with a_hi = tf32(a) (the MMA truncates its fp32 inputs)
           uint32_t ah[16], al2[16];
 #pragma unroll

@@ -447,6 +447,24 @@ __device__ __forceinline__ void i8_lookup(uint32_t (&acc)[NO][4], uint32_t cbase
   }
 }
 
+// Two codebooks at once: their u16-lane contributions meet in one IADD3 per
+// accumulator (12 ALU instructions per 16 lookups instead of 16).
+template <int NO>
+__device__ __forceinline__ void i8_lookup2(uint32_t (&acc)[NO][4], uint32_t cbase0, uint32_t code0, uint32_t cbase1,
+                                           uint32_t code1, int K) {
+  const uint32_t a0 = cbase0 + code0 * 8u, a1 = cbase1 + code1 * 8u;
+#pragma unroll
+  for (int j = 0; j < NO; ++j) {
+    const uint64_t t0 = lds64(a0 + (uint32_t)(j * K * 8));
+    const uint64_t t1 = lds64(a1 + (uint32_t)(j * K * 8));
+    const uint32_t x0 = (uint32_t)t0, y0 = (uint32_t)(t0 >> 32), x1 = (uint32_t)t1, y1 = (uint32_t)(t1 >> 32);
+    acc[j][0] += __byte_perm(x0, 0, 0x4240) + __byte_perm(x1, 0, 0x4240);
+    acc[j][1] += __byte_perm(x0, 0, 0x4341) + __byte_perm(x1, 0, 0x4341);
+    acc[j][2] += __byte_perm(y0, 0, 0x4240) + __byte_perm(y1, 0, 0x4240);
+    acc[j][3] += __byte_perm(y0, 0, 0x4341) + __byte_perm(y1, 0, 0x4341);
+  }
+}
+
 // int8: NO chunks of 8 columns per thread (MT = 8 * NO); biased bytes (q + 128)
 // summed as u16 pairs, widened every 256 codebooks when WIDE.
 template <int NO, bool WIDE, int T>
@@ -500,9 +518,11 @@ __global__ void __launch_bounds__(T, T <= 128 ? 4 : 1)
           if (c0 + 32 <= ce) wn = rc.load16(c0 + 16);
           bad |= codes_bad(w, K, pow2);
 #pragma unroll
-          for (int s = 0; s < 16; ++s) {
-            const uint32_t code = code_byte(w, s);
-            i8_lookup<NO>(acc, sbase + (uint32_t)(c0 + s) * cstep, pow2 ? (code & (uint32_t)(K - 1)) : min(code, (uint32_t)(K - 1)), K);
+          for (int s = 0; s < 16; s += 2) {
+            uint32_t k0 = code_byte(w, s), k1 = code_byte(w, s + 1);
+            k0 = pow2 ? (k0 & (uint32_t)(K - 1)) : min(k0, (uint32_t)(K - 1));
+            k1 = pow2 ? (k1 & (uint32_t)(K - 1)) : min(k1, (uint32_t)(K - 1));
+            i8_lookup2<NO>(acc, sbase + (uint32_t)(c0 + s) * cstep, k0, sbase + (uint32_t)(c0 + s + 1) * cstep, k1, K);
           }
         }
       }
