@@ -326,10 +326,12 @@ __device__ __forceinline__ void stage_i8_slice(uint2* qsm, const int8_t* __restr
 
 // One unit of the row-parallel f32 gather: T rows (thread = row) x 2*NP columns
 // starting at m0, the m-tile's table slice staged at sbase ([c][chunk][k] pairs).
-template <int NP, int T>
+// KC = K when it is a compile-time constant (16: every BASELINE shape), so the
+// NP lookups of a codebook are one address and NP immediate offsets; 0 = runtime K.
+template <int NP, int T, int KC>
 __device__ __forceinline__ void f32_rows_unit(const GatherArgs& g, uint32_t sbase, int m0, int64_t rb, bool v16,
                                               int pow2, bool& bad) {
-  const int K = g.K, C = g.C;
+  const int K = KC > 0 ? KC : g.K, C = g.C;
   const uint32_t cstep = (uint32_t)(NP * K * 8);  // bytes per codebook
   const int64_t row = rb * T + threadIdx.x;
   const bool live = row < g.n;
@@ -337,6 +339,10 @@ __device__ __forceinline__ void f32_rows_unit(const GatherArgs& g, uint32_t sbas
   uint64_t acc[NP];
 #pragma unroll
   for (int j = 0; j < NP; ++j) acc[j] = 0ull;  // (+0.0f, +0.0f)
+  auto clamp = [&](uint32_t code) -> uint32_t {
+    if constexpr (KC > 0 && (KC & (KC - 1)) == 0) return code & (uint32_t)(KC - 1);
+    return pow2 ? (code & (uint32_t)(K - 1)) : min(code, (uint32_t)(K - 1));
+  };
   if (g.code_bits == 8) {
     RowCodes rc{g.codes + rr * g.code_stride, v16};
     int c0 = 0;
@@ -347,11 +353,10 @@ __device__ __forceinline__ void f32_rows_unit(const GatherArgs& g, uint32_t sbas
       const uint4 w = wn;
       if (c0 + 32 <= C) wn = rc.load16(c0 + 16);
       bad |= codes_bad(w, K, pow2);
+      const uint32_t cb = sbase + (uint32_t)c0 * cstep;
 #pragma unroll
       for (int s = 0; s < 16; ++s) {
-        uint32_t code = code_byte(w, s);
-        code = pow2 ? (code & (uint32_t)(K - 1)) : min(code, (uint32_t)(K - 1));
-        const uint32_t a = sbase + (uint32_t)(c0 + s) * cstep + code * 8u;
+        const uint32_t a = cb + (uint32_t)s * cstep + clamp(code_byte(w, s)) * 8u;
 #pragma unroll
         for (int j = 0; j < NP; ++j) fadd2(acc[j], lds64(a + (uint32_t)(j * K * 8)));
       }
@@ -377,39 +382,58 @@ __device__ __forceinline__ void f32_rows_unit(const GatherArgs& g, uint32_t sbas
   if (!live) return;
   int64_t obase, ocs;
   out_row(g, row, obase, ocs);
-  const bool vrow = ocs == 1 && (g.M & 3) == 0 && (reinterpret_cast<uintptr_t>(g.out) & 15) == 0;
+  float v[2 * NP];
 #pragma unroll
-  for (int j = 0; j < NP; j += 2) {
-    float v[4];
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(v[0]), "=f"(v[1]) : "l"(acc[j]));
-    if (j + 1 < NP) {
-      asm("mov.b64 {%0, %1}, %2;" : "=f"(v[2]), "=f"(v[3]) : "l"(acc[j + 1]));
-    } else {
-      v[2] = v[3] = 0.f;
+  for (int j = 0; j < NP; ++j) asm("mov.b64 {%0, %1}, %2;" : "=f"(v[2 * j]), "=f"(v[2 * j + 1]) : "l"(acc[j]));
+  if (m0 + 2 * NP <= g.M) {
+    // full tile: the bias / activation branches are uniform and taken once per tile
+    if (g.bias) {
+      if ((reinterpret_cast<uintptr_t>(g.bias) & 7) == 0) {
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+          const float2 b = __ldg(reinterpret_cast<const float2*>(g.bias + m0) + j);
+          v[2 * j] = __fadd_rn(v[2 * j], b.x);
+          v[2 * j + 1] = __fadd_rn(v[2 * j + 1], b.y);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2 * NP; ++e) v[e] = __fadd_rn(v[e], __ldg(g.bias + m0 + e));
+      }
     }
-    const int col = m0 + 2 * j;
-    const int ncol = j + 1 < NP ? 4 : 2;
+    if (g.act == LUT_ACT_RELU) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) v[e] = (e < ncol && col + e < g.M) ? f32_epilogue(g, v[e], col + e) : 0.f;
-    if (vrow && ncol == 4 && col + 3 < g.M) {
-      *reinterpret_cast<float4*>(g.out + obase + col) = make_float4(v[0], v[1], v[2], v[3]);
+      for (int e = 0; e < 2 * NP; ++e) v[e] = fmaxf(v[e], 0.0f);
+    } else if (g.act == LUT_ACT_GELU) {
+#pragma unroll
+      for (int e = 0; e < 2 * NP; ++e) v[e] = gelu_erf(v[e]);
+    }
+    float* o = g.out + obase + (int64_t)m0 * ocs;
+    if (ocs == 1 && NP >= 2 && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+#pragma unroll
+      for (int e = 0; e + 3 < 2 * NP; e += 4) *reinterpret_cast<float4*>(o + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+    } else if (ocs == 1 && ((reinterpret_cast<uintptr_t>(o) & 7) == 0)) {
+#pragma unroll
+      for (int e = 0; e < 2 * NP; e += 2) *reinterpret_cast<float2*>(o + e) = make_float2(v[e], v[e + 1]);
     } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (e < ncol && col + e < g.M) g.out[obase + (int64_t)(col + e) * ocs] = v[e];
+      for (int e = 0; e < 2 * NP; ++e) o[(int64_t)e * ocs] = v[e];
     }
+    return;
   }
+#pragma unroll
+  for (int e = 0; e < 2 * NP; ++e)
+    if (m0 + e < g.M) g.out[obase + (int64_t)(m0 + e) * ocs] = f32_epilogue(g, v[e], m0 + e);
 }
 
 // Thread block of T threads; NP chunks of 2 f32 columns per thread (MT = 2 * NP).
-template <int NP, int T>
+template <int NP, int T, int KC>
 __global__ void __launch_bounds__(T, T <= 128 ? 4 : 1)
     gather_f32_rows(GatherArgs g, const float* __restrict__ table, int64_t band_rb) {
   extern __shared__ uint2 tsm[];  // [C][NP][K] float pairs
   constexpr int MT = 2 * NP;
   const int nmt = (g.M + MT - 1) / MT;
   const int64_t nrb = (g.n + T - 1) / T;
-  const int K = g.K, C = g.C;
+  const int K = KC > 0 ? KC : g.K, C = g.C;
   const int pow2 = (K & (K - 1)) == 0;
   const bool v16 = g.code_bits == 8 && (g.code_stride & 15) == 0 && (reinterpret_cast<uintptr_t>(g.codes) & 15) == 0;
   const uint32_t sbase = smem_u32(tsm);
@@ -428,7 +452,7 @@ __global__ void __launch_bounds__(T, T <= 128 ? 4 : 1)
       if (cur < 0) grid_dependency_wait();  // the table slice is staged while the encode finishes
       cur = mt;
     }
-    f32_rows_unit<NP, T>(g, sbase, m0, rb, v16, pow2, bad);
+    f32_rows_unit<NP, T, KC>(g, sbase, m0, rb, v16, pow2, bad);
   }
   if (bad && g.err) atomicMax(g.err, (int)LUT_ERR_CORRUPTION);
 }
@@ -667,10 +691,22 @@ static int launch_rows(void (*kern)(GatherArgs, const T*, int64_t), int nmt, siz
 // Rows per CTA: 512 (16 warps hide the LDS latency) unless that leaves SMs idle.
 static bool small_rows(int64_t n, int nmt) { return (n + 511) / 512 * (int64_t)nmt < 2 * (int64_t)num_sms(); }
 
+template <int NP, int KC>
+static int launch_f32_k(int nmt, size_t smem, const GatherArgs& g, const float* table, cudaStream_t stream, int th) {
+#ifdef LUTGPU_PROBES
+  if (th == 128) return launch_rows<float, 128>(gather_f32_rows<NP, 128, KC>, nmt, smem, g, table, stream);
+  if (th == 256) return launch_rows<float, 256>(gather_f32_rows<NP, 256, KC>, nmt, smem, g, table, stream);
+  if (th == 1024) return launch_rows<float, 1024>(gather_f32_rows<NP, 1024, KC>, nmt, smem, g, table, stream);
+#else
+  (void)th;
+#endif
+  return launch_rows<float, 512>(gather_f32_rows<NP, 512, KC>, nmt, smem, g, table, stream);
+}
+
 template <int NP>
-static int launch_f32(int nmt, size_t smem, const GatherArgs& g, const float* table, cudaStream_t stream, bool small) {
-  return small ? launch_rows<float, 128>(gather_f32_rows<NP, 128>, nmt, smem, g, table, stream)
-               : launch_rows<float, 512>(gather_f32_rows<NP, 512>, nmt, smem, g, table, stream);
+static int launch_f32(int nmt, size_t smem, const GatherArgs& g, const float* table, cudaStream_t stream, int th) {
+  return g.K == 16 ? launch_f32_k<NP, 16>(nmt, smem, g, table, stream, th)
+                   : launch_f32_k<NP, 0>(nmt, smem, g, table, stream, th);
 }
 
 int gather_f32_strided(const uint8_t* codes, int code_bits, int64_t code_stride, int64_t n, int C, int K, int M,
@@ -697,20 +733,26 @@ int gather_f32_strided(const uint8_t* codes, int code_bits, int64_t code_stride,
     return LUT_OK;
   }
   int nmt = (M + 2 * NP - 1) / (2 * NP);
-  bool small = small_rows(n, nmt);
-  // few rows: narrower slices and more CTAs until every SM holds several (the
-  // per-row lookup chains are latency-bound at 2 warps per scheduler)
-  while (small && NP > 1 && (n + 127) / 128 * (int64_t)nmt < 4 * (int64_t)num_sms()) {
+  // 512-row CTAs (16 warps hide the LDS latency); few rows: narrower slices until
+  // there are >= 1.5 units per SM (tools/f32_sweep.py, graph-timed on B200:
+  // configs[0] 21.1 -> 11.7 us, the configs[2] convs 16-19 -> 15-16 us)
+  while (NP > 1 && (n + 511) / 512 * (int64_t)nmt * 2 < 3 * (int64_t)num_sms()) {
     NP /= 2;
     nmt = (M + 2 * NP - 1) / (2 * NP);
   }
+  int th = 512;
+  if (const char* e = probe_env("LUTGPU_F32_NP")) {
+    NP = atoi(e);
+    nmt = (M + 2 * NP - 1) / (2 * NP);
+  }
+  if (const char* e = probe_env("LUTGPU_F32_T")) th = atoi(e);
   const size_t smem = per_chunk * NP;
   int st = LUT_OK;
   switch (NP) {
-    case 8: st = launch_f32<8>(nmt, smem, g, table, stream, small); break;
-    case 4: st = launch_f32<4>(nmt, smem, g, table, stream, small); break;
-    case 2: st = launch_f32<2>(nmt, smem, g, table, stream, small); break;
-    default: st = launch_f32<1>(nmt, smem, g, table, stream, small); break;
+    case 8: st = launch_f32<8>(nmt, smem, g, table, stream, th); break;
+    case 4: st = launch_f32<4>(nmt, smem, g, table, stream, th); break;
+    case 2: st = launch_f32<2>(nmt, smem, g, table, stream, th); break;
+    default: st = launch_f32<1>(nmt, smem, g, table, stream, th); break;
   }
   if (st != LUT_OK) return st;
   LUT_CHECK_LAUNCH("gather_f32_rows");
