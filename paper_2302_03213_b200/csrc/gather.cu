@@ -491,14 +491,14 @@ __device__ __forceinline__ void i8_lookup2(uint32_t (&acc)[NO][4], uint32_t cbas
 
 // int8: NO chunks of 8 columns per thread (MT = 8 * NO); biased bytes (q + 128)
 // summed as u16 pairs, widened every 256 codebooks when WIDE.
-template <int NO, bool WIDE, int T>
+template <int NO, bool WIDE, int T, int KC>
 __global__ void __launch_bounds__(T, T <= 128 ? 4 : 1)
     gather_i8_rows(GatherArgs g, const int8_t* __restrict__ q8, int64_t band_rb) {
   extern __shared__ uint2 qsm[];  // [C][NO][K] x 8 biased bytes
   constexpr int MT = 8 * NO;
   const int nmt = (g.M + MT - 1) / MT;
   const int64_t nrb = (g.n + T - 1) / T;
-  const int K = g.K, C = g.C;
+  const int K = KC > 0 ? KC : g.K, C = g.C;  // KC: compile-time K (immediate lookup offsets)
   const int pow2 = (K & (K - 1)) == 0;
   const bool v16 = g.code_bits == 8 && (g.code_stride & 15) == 0 && (reinterpret_cast<uintptr_t>(g.codes) & 15) == 0;
   const uint32_t sbase = smem_u32(qsm);
@@ -759,10 +759,16 @@ int gather_f32_strided(const uint8_t* codes, int code_bits, int64_t code_stride,
   return LUT_OK;
 }
 
+template <int NO, bool WIDE, int KC>
+static int launch_i8_k(int nmt, size_t smem, const GatherArgs& g, const int8_t* q, cudaStream_t stream, bool small) {
+  return small ? launch_rows<int8_t, 128>(gather_i8_rows<NO, WIDE, 128, KC>, nmt, smem, g, q, stream)
+               : launch_rows<int8_t, 512>(gather_i8_rows<NO, WIDE, 512, KC>, nmt, smem, g, q, stream);
+}
+
 template <int NO, bool WIDE>
 static int launch_i8(int nmt, size_t smem, const GatherArgs& g, const int8_t* q, cudaStream_t stream, bool small) {
-  return small ? launch_rows<int8_t, 128>(gather_i8_rows<NO, WIDE, 128>, nmt, smem, g, q, stream)
-               : launch_rows<int8_t, 512>(gather_i8_rows<NO, WIDE, 512>, nmt, smem, g, q, stream);
+  return g.K == 16 ? launch_i8_k<NO, WIDE, 16>(nmt, smem, g, q, stream, small)
+                   : launch_i8_k<NO, WIDE, 0>(nmt, smem, g, q, stream, small);
 }
 
 int gather_i8_strided(const uint8_t* codes, int code_bits, int64_t code_stride, int64_t n, int C, int K, int M,
