@@ -457,6 +457,11 @@ __global__ void __launch_bounds__(T, T <= 128 ? 4 : 1)
   if (bad && g.err) atomicMax(g.err, (int)LUT_ERR_CORRUPTION);
 }
 
+// Per 8-column chunk the accumulators hold sx = sum of the raw words of bytes
+// 0-3, ox = sum of their odd bytes {1, 3} as u16 lanes, and sy / oy for bytes
+// 4-7.  Since w = even(w) + (odd(w) << 8) as integers, the even-byte sums
+// follow exactly (mod 2^32, every lane < 2^16) as sx - (ox << 8) once per
+// 256-codebook block (i8_even): one PRMT per word instead of two.
 template <int NO>
 __device__ __forceinline__ void i8_lookup(uint32_t (&acc)[NO][4], uint32_t cbase, uint32_t code, int K) {
   const uint32_t a = cbase + code * 8u;
@@ -464,15 +469,14 @@ __device__ __forceinline__ void i8_lookup(uint32_t (&acc)[NO][4], uint32_t cbase
   for (int j = 0; j < NO; ++j) {
     const uint64_t t = lds64(a + (uint32_t)(j * K * 8));
     const uint32_t w0 = (uint32_t)t, w1 = (uint32_t)(t >> 32);
-    acc[j][0] += __byte_perm(w0, 0, 0x4240);  // biased bytes 0, 2 -> u16 lanes
-    acc[j][1] += __byte_perm(w0, 0, 0x4341);  // bytes 1, 3
-    acc[j][2] += __byte_perm(w1, 0, 0x4240);
+    acc[j][0] += w0;
+    acc[j][1] += __byte_perm(w0, 0, 0x4341);  // biased bytes 1, 3 -> u16 lanes
+    acc[j][2] += w1;
     acc[j][3] += __byte_perm(w1, 0, 0x4341);
   }
 }
 
-// Two codebooks at once: their u16-lane contributions meet in one IADD3 per
-// accumulator (12 ALU instructions per 16 lookups instead of 16).
+// Two codebooks at once: their contributions meet in one IADD3 per accumulator.
 template <int NO>
 __device__ __forceinline__ void i8_lookup2(uint32_t (&acc)[NO][4], uint32_t cbase0, uint32_t code0, uint32_t cbase1,
                                            uint32_t code1, int K) {
@@ -482,10 +486,20 @@ __device__ __forceinline__ void i8_lookup2(uint32_t (&acc)[NO][4], uint32_t cbas
     const uint64_t t0 = lds64(a0 + (uint32_t)(j * K * 8));
     const uint64_t t1 = lds64(a1 + (uint32_t)(j * K * 8));
     const uint32_t x0 = (uint32_t)t0, y0 = (uint32_t)(t0 >> 32), x1 = (uint32_t)t1, y1 = (uint32_t)(t1 >> 32);
-    acc[j][0] += __byte_perm(x0, 0, 0x4240) + __byte_perm(x1, 0, 0x4240);
+    acc[j][0] += x0 + x1;
     acc[j][1] += __byte_perm(x0, 0, 0x4341) + __byte_perm(x1, 0, 0x4341);
-    acc[j][2] += __byte_perm(y0, 0, 0x4240) + __byte_perm(y1, 0, 0x4240);
+    acc[j][2] += y0 + y1;
     acc[j][3] += __byte_perm(y0, 0, 0x4341) + __byte_perm(y1, 0, 0x4341);
+  }
+}
+
+// raw word sums -> even-byte u16 lanes: acc = {bytes {0,2}, {1,3}, {4,6}, {5,7}}
+template <int NO>
+__device__ __forceinline__ void i8_even(uint32_t (&acc)[NO][4]) {
+#pragma unroll
+  for (int j = 0; j < NO; ++j) {
+    acc[j][0] -= acc[j][1] << 8;
+    acc[j][2] -= acc[j][3] << 8;
   }
 }
 
@@ -555,6 +569,7 @@ __global__ void __launch_bounds__(T, T <= 128 ? 4 : 1)
         bad |= code >= (uint32_t)K;
         i8_lookup<NO>(acc, sbase + (uint32_t)c0 * cstep, min(code, (uint32_t)(K - 1)), K);
       }
+      i8_even<NO>(acc);
       if constexpr (WIDE) {
         const int b128 = 128 * (ce - cb);
 #pragma unroll
