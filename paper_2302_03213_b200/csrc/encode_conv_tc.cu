@@ -89,28 +89,31 @@ __device__ __forceinline__ void ct_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "memory");
 }
 
-// Screen one (pixel, channel): dv = the 16 3xTF32 dots from TMEM, a = the
-// fp32 patch, asq = |a|^2, ax = [|p_k|^2 x16, max|p|^2, 2^-15 max|p| (up)],
-// cp = the channel's fp32 centroids.  Returns the encode_hard index.
+// Screen one (pixel, channel): dv = the 16 3xTF32 values D_k = a.p_k - |p_k|^2/2
+// from TMEM (the MMA's K column 9 holds A = 1 against B = -|p_k|^2/2, so
+// D_k = -d~_k / 2), a = the fp32 patch, asq = |a|^2, ax = [|p_k|^2 x16, max|p|^2,
+// 2^-15 max|p| (up)], cp = the channel's fp32 centroids.  Returns the encode_hard index.
 __device__ __forceinline__ int conv_screen(const uint32_t (&dv)[16], const float (&a)[9], float asq, const float* ax,
                                           const float* cp, float tau_c, int* near_tie, bool live) {
   constexpr int V = 9, K = 16;
-  // D = 2^-15 |a| max|p_k| + 2^-21 (|a|^2 + max|p_k|^2): the 3xTF32 dot error is
-  // <= 3 * 2^-20 sum|a_j p_j| (the dropped a_lo.p_lo and the truncations of the
-  // low parts) + the fp32 accumulation over 6 chained MMAs; doubled for the -2
-  // factor, with a 2x margin
+  // |D_k + d_k / 2| <= hwd / 2 with hwd = 2^-15 |a| max|p_k| + 2^-19 (|a|^2 + max|p_k|^2):
+  // the 3xTF32 dot error <= 3 * 2^-20 sum|a_j p_j| (the dropped a_lo.p_lo and the
+  // truncations of the low parts), |p_k|^2 / 2 split hi + lo (the lo part truncated:
+  // 2^-21 |p_k|^2) and the fp32 accumulation over 6 chained MMAs, with a 2x margin;
+  // every k with D_k < max D - hwd is provably not the argmin.  The absolute floor
+  // keeps the bound positive for vanishing operands.
   const float al = __fmul_ru(__fsqrt_ru(asq), 1.0000002f);
-  const float hwd = fmaf(al, ax[K + 1], 4.7683716e-7f * (asq + ax[K]));
+  const float hwd = fmaf(al, ax[K + 1], fmaf(1.9073486e-6f, asq + ax[K], 1e-30f));
   float dt[16];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) dt[k] = fmaf(-2.0f, __uint_as_float(dv[k]), ax[k]);
-  float mn = fminf(fminf(dt[0], dt[1]), fminf(dt[2], dt[3]));
+  for (int k = 0; k < 16; ++k) dt[k] = __uint_as_float(dv[k]);
+  float mx = fmaxf(fmaxf(dt[0], dt[1]), fmaxf(dt[2], dt[3]));
 #pragma unroll
-  for (int k = 4; k < 16; k += 4) mn = fminf(mn, fminf(fminf(dt[k], dt[k + 1]), fminf(dt[k + 2], dt[k + 3])));
-  const float thr = __fadd_ru(mn, 2.0f * hwd);
+  for (int k = 4; k < 16; k += 4) mx = fmaxf(mx, fmaxf(fmaxf(dt[k], dt[k + 1]), fmaxf(dt[k + 2], dt[k + 3])));
+  const float thr = __fsub_rd(mx, hwd);
   uint32_t mask = 0u;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) mask |= (dt[k] <= thr) ? (1u << k) : 0u;
+  for (int k = 0; k < 16; ++k) mask |= (dt[k] >= thr) ? (1u << k) : 0u;
   if (mask != 0u && (mask & (mask - 1u)) == 0u) return __ffs((int)mask) - 1;
   // refine the candidates in fp32 (d = fma(-2, a.p, |p|^2), encode.cu's formulation)
   float best = FLT_MAX, second = FLT_MAX;
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(kCtThreads, 1) encode_conv_tc_kernel(const Con
     const int r_local = grp * 128 + q * 32 + lane;  // pixel within the unit
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(grp * 128);
     const float tau_c = (4.0f * V + 16.0f) * 5.9604645e-8f;
-    uint32_t dphase[2] = {0u, 0u};
+    uint32_t dphase = 0u;  // bit b: parity of dfull[grp][b]
     int cur_g = -1;
     int it = 0;
     for (int64_t u = blockIdx.x; u < p.nunits; u += gridDim.x, ++it) {
@@ -238,6 +241,7 @@ __global__ void __launch_bounds__(kCtThreads, 1) encode_conv_tc_kernel(const Con
           const int c = g * kCtCh + ch;
           float v = 0.0f;
           if (c < p.cin && kk < V) v = __ldg(p.prep + (size_t)c * p.S + k * V + kk);
+          if (c < p.cin && kk == V) v = -0.5f * __ldg(p.prep + (size_t)c * p.S + K * V + k);  // against A = 1
           const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);  // tf32(p), then p - tf32(p)
           const int off = k * 32 + ((((kk >> 2) ^ (k & 7)) << 2) | (kk & 3));
           reinterpret_cast<float*>(btiles + (2 * ch) * kCtBTile)[off] = hi;
@@ -303,7 +307,7 @@ __global__ void __launch_bounds__(kCtThreads, 1) encode_conv_tc_kernel(const Con
           uint32_t ah[16], al2[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const float v = j < V ? a[j] : 0.0f;
+            const float v = j < V ? a[j] : (j == V ? 1.0f : 0.0f);  // column 9: the -|p_k|^2/2 term
             const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
             ah[j] = __float_as_uint(hi);
             al2[j] = __float_as_uint(v - hi);
@@ -342,8 +346,8 @@ __global__ void __launch_bounds__(kCtThreads, 1) encode_conv_tc_kernel(const Con
         }
         if (cl > 0) {
           const int pc = cl - 1, ps = pc & 1;
-          mbar_wait(&dfull[grp * 2 + ps], dphase[ps]);
-          dphase[ps] ^= 1u;
+          mbar_wait(&dfull[grp * 2 + ps], (dphase >> ps) & 1u);
+          dphase ^= 1u << ps;
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           uint32_t dv[16];
           ct_ld16(lane_base + (uint32_t)(ps * 48 + 32), dv);
