@@ -749,9 +749,11 @@ int gather_f32_strided(const uint8_t* codes, int code_bits, int64_t code_stride,
   }
   int nmt = (M + 2 * NP - 1) / (2 * NP);
   // 512-row CTAs (16 warps hide the LDS latency); few rows: narrower slices until
-  // there are >= 1.5 units per SM (tools/f32_sweep.py, graph-timed on B200:
-  // configs[0] 21.1 -> 11.7 us, the configs[2] convs 16-19 -> 15-16 us)
-  while (NP > 1 && (n + 511) / 512 * (int64_t)nmt * 2 < 3 * (int64_t)num_sms()) {
+  // there are >= 1.5 units per SM, or >= 4 when a unit is heavy (C * NP > 512:
+  // the last wave's imbalance) — tools/f32_sweep.py, graph-timed on B200:
+  // configs[0] 21.1 -> 11.7 us, the configs[2] convs 16-19 -> 15-16 us,
+  // configs[1] FFN2 59 -> 55 us
+  while (NP > 1 && (n + 511) / 512 * (int64_t)nmt * 2 < (C * NP > 512 ? 8 : 3) * (int64_t)num_sms()) {
     NP /= 2;
     nmt = (M + 2 * NP - 1) / (2 * NP);
   }

@@ -70,6 +70,8 @@ def timeit(fn, reps=7, cold=True):
 
 
 SHAPES = [
+    ("ffn1", 4096, 24, 16, 3072, 0, True),
+    ("ffn2", 4096, 96, 16, 768, 0, True),
     ("cfg1", 1024, 48, 16, 768, 0, False),
     ("conv1", 256 * 1024, 16, 16, 16, 1024, True),
     ("conv2", 256 * 256, 32, 16, 32, 256, True),

@@ -1,5 +1,5 @@
-"""One lut_gather_f32 call per small BASELINE shape (configs[0], the three
-configs[2] convs) — the launch list an ncu capture of the small gathers needs.
+"""One lut_gather_f32 call per small BASELINE shape (configs[1] FFN pair, configs[0],
+the three configs[2] convs) — the launch list an ncu capture of the small gathers needs.
 
 usage: ncu ... python tools/small_gathers_once.py [lib.so]
 """
@@ -22,6 +22,8 @@ dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(3)
 sp = torch.cuda.current_stream().cuda_stream
 for name, n, c, k, m, hw, epi in [
+    ("ffn1", 4096, 24, 16, 3072, 0, True),
+    ("ffn2", 4096, 96, 16, 768, 0, True),
     ("cfg1", 1024, 48, 16, 768, 0, False),
     ("conv1", 256 * 1024, 16, 16, 16, 1024, True),
     ("conv2", 256 * 256, 32, 16, 32, 256, True),
