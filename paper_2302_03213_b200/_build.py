@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "liblutgpu.so")
-SOURCES = ["capi.cu", "encode.cu", "encode_tc.cu", "encode_conv_tc.cu", "gather.cu", "onehot.cu", "onehot_stream.cu", "table.cu"]
+SOURCES = ["capi.cu", "encode.cu", "encode_tc.cu", "encode_conv_tc.cu", "encode_conv_strip.cu", "gather.cu", "onehot.cu", "onehot_stream.cu", "table.cu"]
 HEADERS = ["common.cuh", "onehot_dev.cuh", "encode_dev.cuh"]
 
 NVCC_FLAGS = [

@@ -894,6 +894,10 @@ int launch_conv_tc(const float* x, int batch, int cin, int h, int w, int stride,
                    const float* prep, int K, uint8_t* codes, int64_t code_stride, int* near_tie, cudaStream_t stream,
                    bool* used);
 
+int launch_conv_strip(const float* x, int batch, int cin, int h, int w, int stride, int pad, int ho, int wo,
+                      const float* prep, int K, uint8_t* codes, int64_t code_stride, int* near_tie,
+                      cudaStream_t stream, bool* used);
+
 int encode_conv_strided(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad,
                         const float* prep, int C, int K, int V, uint8_t* codes, int64_t code_stride, int* near_tie,
                         cudaStream_t stream) {
@@ -905,6 +909,14 @@ int encode_conv_strided(const float* x, int batch, int cin, int h, int w, int kh
   if (kh == 3 && kw == 3 && V == 9 && C == cin && !(force && atoi(force))) {
     bool used = false;
     int st = LUT_OK;
+    const char* strip_env = probe_env("LUTGPU_CONV_STRIP");
+    if (K == 16 && !(strip_env && strip_env[0] == '0')) {
+      // register-tiled pixel strips on the FP32 pipe (encode_conv_strip.cu)
+      st = launch_conv_strip(x, batch, cin, h, w, stride, pad, ho, wo, prep, K, codes, code_stride, near_tie, stream,
+                             &used);
+      if (st != LUT_OK) return st;
+      if (used) return LUT_OK;
+    }
     const char* tc_env = probe_env("LUTGPU_CONV_TC");
     if (K == 16 && !(tc_env && tc_env[0] == '0')) {
       // tensor-core screening (encode_conv_tc.cu)

@@ -1,8 +1,10 @@
-"""GPU: the tensor-core conv encode (csrc/encode_conv_tc.cu, 3xTF32 screening +
-exact refinement) == encode_hard on the im2col patches (pq.py:171-174,
-tensor.py:36-79): configs[2] geometries, partial 512-pixel units and 16-channel
-groups, strides / padding, crafted ties (duplicate centroids -> lowest k),
-exact centroid hits and large / small magnitudes."""
+"""GPU: the 3x3 conv encodes == encode_hard on the im2col patches (pq.py:171-174,
+tensor.py:36-79).  Stride-1 shapes with an even output width run the FP32-pipe
+strip kernel (csrc/encode_conv_strip.cu); the others the tensor-core screen
+(csrc/encode_conv_tc.cu, 3xTF32 + exact refinement) or the plane / generic row
+kernels.  configs[2] geometries, partial units and channel groups, strides /
+padding, crafted ties (duplicate centroids -> lowest k), exact centroid hits and
+large / small magnitudes."""
 
 import numpy as np
 import pytest
@@ -37,7 +39,11 @@ def _conv_codes(L, x, books, stride, pad):
 
 
 @pytest.mark.parametrize("b,cin,hw,stride,pad", [(4, 16, 32, 1, 1), (6, 32, 16, 1, 1), (20, 64, 8, 1, 1),
-                                                 (3, 24, 16, 1, 1), (5, 16, 16, 2, 1), (9, 40, 8, 1, 0)])
+                                                 (3, 24, 16, 1, 1), (5, 16, 16, 2, 1), (9, 40, 8, 1, 0),
+                                                 # strip kernel: 2-pixel strips (Wo = 6), odd channel / image tails
+                                                 (7, 13, 6, 1, 1), (21, 9, 8, 1, 1), (3, 8, 12, 1, 0), (2, 5, 18, 1, 1),
+                                                 # odd output width / pad 2: generic kernels
+                                                 (3, 8, 7, 1, 1), (2, 8, 8, 1, 2)])
 def test_conv_tc_encode_random(L, b, cin, hw, stride, pad):
     rng = O.make_rng(b * cin + hw)
     x = np.abs(rng.standard_normal((b, cin, hw, hw))).astype(F32)
@@ -46,7 +52,8 @@ def test_conv_tc_encode_random(L, b, cin, hw, stride, pad):
     np.testing.assert_array_equal(got, O.encode_hard(O.im2col(x, 3, 3, stride, pad), books))
 
 
-def test_conv_tc_encode_crafted(L):
+@pytest.mark.parametrize("stride", [1, 2])
+def test_conv_tc_encode_crafted(L, stride):
     rng = O.make_rng(4242)
     b, cin, hw = 8, 32, 16
     x = np.abs(rng.standard_normal((b, cin, hw, hw))).astype(F32)
@@ -62,11 +69,13 @@ def test_conv_tc_encode_crafted(L):
     for i in range(40):
         bi, c, k = i % b, i % cin, i % 16
         y, xx = 1 + (i * 3) % (hw - 2), 1 + (i * 5) % (hw - 2)
+        if stride == 2:  # patch centres of the stride-2 output grid (pad 1): even coordinates
+            y, xx = max(2, y & ~1), max(2, xx & ~1)
         x[bi, c, y - 1:y + 2, xx - 1:xx + 2] = books[c, k].reshape(3, 3)
     # duplicated-centroid hits (exact ties)
-    x[0, 0, 4:7, 4:7] = books[0, 3].reshape(3, 3)
-    x[1, 1, 8:11, 8:11] = books[1, 0].reshape(3, 3)
-    got, near = _conv_codes(L, x, books, 1, 1)
-    want = O.encode_hard(O.im2col(x, 3, 3, 1, 1), books)
+    x[0, 0, 3:6, 3:6] = books[0, 3].reshape(3, 3)      # centre (4, 4)
+    x[1, 1, 7:10, 7:10] = books[1, 0].reshape(3, 3)    # centre (8, 8)
+    got, near = _conv_codes(L, x, books, stride, 1)
+    want = O.encode_hard(O.im2col(x, 3, 3, stride, 1), books)
     np.testing.assert_array_equal(got, want)
     assert near >= 2  # the exact ties were re-decided in f64
