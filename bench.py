@@ -780,6 +780,17 @@ def main_stack(args):
         dist.destroy_process_group()
     if rank != 0:
         return
+    # DRAM bytes per step from the committed ncu launch list of this workload's default arguments
+    traffic, traffic_src = None, None
+    default_table = "f32" if wl in ("cfg1", "cfg3") else "i8"
+    if not args.per_table_scales and args.table == default_table and args.scale_mtile == -1:
+        for rnd in ("r02",):
+            try:
+                with open(os.path.join(ROOT, "profiles", rnd, "ncu_traffic_stacks.json")) as f:
+                    traffic = json.load(f)["workloads"][wl]["dram_bytes_per_step"]
+                traffic_src = f"profiles/{rnd}/ncu_traffic_stacks.json"
+            except (OSError, KeyError, ValueError):
+                pass
     line = {"metric": METRIC, "value": rows * world / (ms / 1e3), "unit": f"{unit_rows}/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
@@ -792,14 +803,16 @@ def main_stack(args):
                        **({"int8_scales": "per (m-tile)" if args.per_table_scales else "per (codebook, m-tile)"}
                           if wl == "cfg2" else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": None, "kernel": "LUT layers (encode+gather)",
+                         "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "kernel": "LUT layers (encode+gather)",
                          "peak_kind": peak_kind, "algorithmic_bytes": lut_bytes, "lut_ms_eager": lut_ms,
                          "lut_layers": len(marks),
                          "survey_bound": {"t_bound_ms": t_bound * 1e3,
                                           "binding": max(bound_terms, key=bound_terms.get),
                                           "terms_ms": {k_: v_ * 1e3 for k_, v_ in bound_terms.items()},
                                           "frac_of_step": t_bound * 1e3 / ms}},
-            "clocks": clocks.summary(), "gpu_launches": None,
+            # our kernels in the timed region: one encode + one gather launch per LUT layer and step
+            "clocks": clocks.summary(), "gpu_launches": 2 * len(marks) * args.steps,
             "e2e": {"value": rows * world / e2e_s, "unit": f"{unit_rows}/s", "h2d_bytes_per_step": x.numel() * 4,
                     "d2h_bytes_per_step": y0.numel() * 4},
             "cpu_baseline": cpu}
