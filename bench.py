@@ -377,12 +377,14 @@ def main():
             return
         ref = cpu_reference(d, m, v, k, integer, rows_per_core=args.cpu_rows or (4096 if integer else 2048),
                             steps=max(1, args.steps), warmup=max(0, args.warmup))
-        config["rows_sampled_per_step"] = ref["rows_sampled"]
+        # config is key-for-key the GPU arm's (the driver compares the two lines' configs); the CPU
+        # sample size travels beside it and in cpu_baseline.sample
         eff = 2.0 * d * m * ref["value"] / 1e9
         line = {"impl": "reference", "metric": METRIC, "value": ref["value"], "unit": UNIT, "n_gpus": args.gpus,
                 "steps": ref["steps"], "warmup": ref["warmup"], "ms_per_step": ref["seconds_per_step"] * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
-                "data": "synthetic", "config": config, "effective_gops": eff,
+                "data": "synthetic", "config": config, "rows_sampled_per_step": ref["rows_sampled"],
+                "effective_gops": eff,
                 "cpu_baseline": {k_: ref[k_] for k_ in ("value", "unit", "cores", "kind", "sample")},
                 "one_core": ref.get("one_core"), "linearity": ref.get("linearity"),
                 "plan_8192_16": ref.get("plan_8192_16"),
@@ -416,7 +418,6 @@ def main():
     near = torch.zeros(1, dtype=torch.int32, device=dev)
     hbm_peak, _, peak_kind = peaks()
     run = Cfg5(L, lib, dev, a, codes, out, near, d, m, v, k, integer, args.gather, args.digits)
-    config["gather"] = run.engine
     with ClockSampler(local) as clocks:
         ms_step, enc_ms, gat_ms = run.time(args.steps, args.warmup, world)
     in_dist = dist.is_available() and dist.is_initialized()
@@ -530,7 +531,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if not integer else "f32-encode/int8-table/int32-acc",
             "data": "synthetic (seeded torch.randn on device; random-init centroids/weights)",
-            "config": config, "effective_gops": eff_gops,
+            "config": config, "engine": run.engine, "effective_gops": eff_gops,
             "near_ties_gap_lt_1e6": near_1e6,
             "near_ties_gap_lt_1e6_rate": None if near_1e6 is None else near_1e6 / (n * c),
             "f64_redecisions": redecided // max(1, args.steps), "f64_redecision_rate": redecided / (n * c * args.steps),

@@ -224,7 +224,7 @@ def test_bench_reference_arm_small():
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0 and line["steps"] == 2 and line["warmup"] == 1
     assert line["one_core"]["cores"] == 1 and "linear" in line["linearity"]
-    assert line["config"]["rows_sampled_per_step"] == line["cpu_baseline"]["cores"] * 64
+    assert line["rows_sampled_per_step"] == line["cpu_baseline"]["cores"] * 64
     assert line["e2e"]["h2d_bytes_per_step"] == 0
 
 
