@@ -90,7 +90,7 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int N, int iters, long long* out
           dd += 256;
         }
       }
-      if ((mode & 256) && !(i & 1)) asm volatile("bar.sync 1, 64;" ::: "memory");  // hand-off from the watcher warp
+      if ((mode & 256) && (!(i & 1) || (mode & 1048576))) asm volatile("bar.sync 1, 64;" ::: "memory");  // hand-off from the watcher warp (1048576: every 4 MMAs)
       if ((mode & 8) && ((mode & 64) ? !(i & 3) : !(i & 1))) {  // poll a completed barrier every 8 (or 16) MMAs
         uint32_t ok = 0;
         if (mode & 128) {  // poll a plain SMEM flag word (LSU path) instead of an mbarrier
@@ -122,7 +122,7 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int N, int iters, long long* out
         asm volatile(SP_STAGE(2)::"r"(dd), "r"(t + a), "l"(bb), "r"(idesc), "r"((uint32_t)((i & 7) != 0)),
                      "r"(t + a + 64 - 32 * (uint32_t)(i & 1) + 8 * (uint32_t)(i & 1))
                      : "memory");
-        if ((mode & 4) && (i & 1)) {  // commit every 8 MMAs (multicast to both CTAs' barrier 2)
+        if ((mode & 4) && ((i & 1) || (mode & 1048576))) {  // commit every 8 MMAs (1048576: every 4) (multicast to both CTAs' barrier 2)
           asm volatile(
               "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
               "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
@@ -151,7 +151,7 @@ __global__ void __cluster_dims__(2, 1, 1) bench(int N, int iters, long long* out
     stop = 1;
   } else if (warp == 2 && (mode & 256) && (rank == 0 || G == 1)) {
     // watcher: polls the (completed) barrier, then releases the issuer through a named barrier
-    for (int i = 0; i < iters; i += 2) {
+    for (int i = 0; i < iters; i += (mode & 1048576) ? 1 : 2) {
       uint32_t ok = 0;
       while (!ok)
         asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.relaxed.cluster.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0,1,0,p;\n\t}"
@@ -248,7 +248,10 @@ int main() {
   for (int mode : {0, 4, 260, 516, 772 + 8192, 772 + 16384, 772 + 32768, 772 + 8192 + 16384 + 32768, 772, 773, 772 + 65536, 773 + 65536, 773 + 131072, 773 + 65536 + 131072, 772 + 262144,
                    773 + 262144 + 131072, 775 + 65536 + 131072, 775 + 262144 + 131072, 775})
     run<2>(128, 148, mode);
-  for (int n : {128, 256})  // one accumulator at column 256, A ring at 0..239
+  for (int n : {128, 160, 192, 224, 256})  // one accumulator at column 256, A ring at 0..239
     for (int mode : {4, 772 + 4096 + 8192, 773 + 4096 + 8192, 775 + 4096 + 8192}) run<2>(n, 148, mode);
+  // 4-MMA ring stages (commit + watcher hand-off every 4 MMAs): the N = 192 design's 2-K-block stages
+  for (int n : {128, 192})
+    for (int mode : {772 + 4096 + 8192 + 1048576, 773 + 4096 + 8192 + 1048576, 775 + 4096 + 8192 + 1048576}) run<2>(n, 148, mode);
   return 0;
 }
