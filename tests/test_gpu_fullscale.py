@@ -110,3 +110,44 @@ def test_k64_int8_layer_bytes_at_benched_geometry(L):
     q, s = O.quantize_table(O.build_table(w, books))
     want = O.lut_layer_infer(a, books, q=q, scale=s)
     assert got.tobytes() == want.tobytes()
+
+
+def test_fullscale_headline_layer_properties(L):
+    """The benched configs[4] layer itself (2^20 rows, K = 16, int8 tables, 17.2 GB
+    of output) through size-independent properties:
+    * the tensor-core layer output equals the CUDA-core engine's on every one of
+      the 2^20 x 4096 outputs, bitwise (two independent kernels, exact int32 sums:
+      kernels.py:105-135);
+    * per-row checksums are invariant under a row permutation of the input (rows
+      are independent: kernels.py:78-86);
+    * 2048 rows spread over the whole range equal the oracle's bytes."""
+    import torch
+
+    dev = torch.device("cuda", 0)
+    rng = O.make_rng(2020)
+    k, m = 16, 4096
+    books = rng.standard_normal((C, k, V)).astype(F32)
+    w = (rng.standard_normal((D_FULL, m)) / np.sqrt(D_FULL)).astype(F32)
+    lt = L.LutLayer(cfg=L.PqConfig(v=V, k=k), books=books, weight=w, qat=True, gather="tensor")
+    lc = L.LutLayer(cfg=L.PqConfig(v=V, k=k), books=books, weight=w, qat=True, gather="cuda")
+    assert lt.uses_tensor_cores(True) and not lc.uses_tensor_cores(True)
+    ga = torch.Generator(device=dev).manual_seed(7)
+    a = torch.randn((N_FULL, D_FULL), generator=ga, device=dev)
+    out_t = lt.forward_device(a, True)
+    out_c = lc.forward_device(a, True)
+    # bitwise over all 4.3e9 outputs, in row chunks (no 17 GB boolean temporary)
+    for r0 in range(0, N_FULL, 1 << 16):
+        assert torch.equal(out_t[r0:r0 + (1 << 16)], out_c[r0:r0 + (1 << 16)]), f"engines differ in rows {r0}.."
+    del out_c
+    # row independence: a permuted 2^18-row slice gives the permuted rows' checksums
+    sl = slice(3 << 18, 4 << 18)
+    perm = torch.randperm(1 << 18, generator=torch.Generator(device=dev).manual_seed(3), device=dev)
+    sums = out_t[sl].view(torch.int32).to(torch.int64).sum(1)
+    out_p = lt.forward_device(a[sl][perm].contiguous(), True)
+    assert torch.equal(out_p.view(torch.int32).to(torch.int64).sum(1), sums[perm])
+    del out_p
+    # rows spread over the whole range against the oracle
+    idx = torch.arange(0, N_FULL, N_FULL // 2048, device=dev)[:2048]
+    q, s = O.quantize_table(O.build_table(w, books))
+    want = O.lut_layer_infer(a[idx].cpu().numpy(), books, q=q, scale=s)
+    assert out_t[idx].cpu().numpy().tobytes() == want.tobytes()
