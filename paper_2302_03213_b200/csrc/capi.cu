@@ -41,7 +41,7 @@ int onehot_prepare_i8(const int8_t* q, int C, int K, int M, void* image, cudaStr
 int onehot_prepare_f32(const float* t, int C, int K, int M, int digits, void* image, int* err, cudaStream_t stream);
 int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, int K, int M, int digits,
                   const void* image, const float* scales, int scale_mtile, const float* bias, int act, float* out,
-                  int32_t* out_i32, int64_t out_hw, cudaStream_t stream);
+                  int32_t* out_i32, int64_t out_hw, cudaStream_t stream, int pdl = 0);
 int encode_conv_strided(const float* x, int batch, int cin, int h, int w, int kh, int kw, int stride, int pad,
                         const float* prep, int C, int K, int V, uint8_t* codes, int64_t code_stride, int* near_tie,
                         cudaStream_t stream);
@@ -462,7 +462,7 @@ int lut_layer_forward(const lut_layer_desc* L, const float* a, int64_t n, float*
   if (L->onehot_image) {
     const int digits = L->integer ? 1 : L->onehot_digits;
     return onehot_gather(codes_scratch, stride, n, L->c, L->k, L->m, digits, L->onehot_image, L->scales,
-                         L->scale_mtile, L->bias, L->act, out, nullptr, 0, s);
+                         L->scale_mtile, L->bias, L->act, out, nullptr, 0, s, /*pdl=*/1);
   }
   if (L->integer)
     return gather_i8_strided(codes_scratch, 8, stride, n, L->c, L->k, L->m, L->q, L->scales, L->scale_mtile, L->bias,
@@ -491,7 +491,7 @@ int lut_conv_layer_forward(const lut_layer_desc* L, const float* x, int32_t batc
   if (L->onehot_image) {
     const int digits = L->integer ? 1 : L->onehot_digits;
     return onehot_gather(codes_scratch, stride_c, n, L->c, L->k, L->m, digits, L->onehot_image, L->scales,
-                         L->scale_mtile, L->bias, L->act, out, nullptr, (int64_t)ho * wo, s);
+                         L->scale_mtile, L->bias, L->act, out, nullptr, (int64_t)ho * wo, s, /*pdl=*/1);
   }
   if (L->integer)
     return gather_i8_strided(codes_scratch, 8, stride_c, n, L->c, L->k, L->m, L->q, L->scales, L->scale_mtile, L->bias,

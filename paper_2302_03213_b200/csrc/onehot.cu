@@ -531,6 +531,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       int ntile;
       int64_t rt;
       bool first_b = true;
+      bool dep_waited = false;  // the codes come from the preceding encode (programmatic dependent launch)
       while (walk.next(ntile, rt)) {
         if (ntile != cur_ntile) {
           if (!first_b) {
@@ -552,6 +553,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           cur_ntile = ntile;
         }
         mbar_wait(&code_empty[cs], cphase ^ 1);
+        if (!dep_waited) {
+          grid_dependency_wait();  // no-op unless launched as a programmatic dependent
+          dep_waited = true;
+        }
         mbar_arrive_expect_tx(&code_full[cs], (uint32_t)code_tile_bytes);
         for (int bx = 0; bx < p.code_boxes; ++bx)
           tma_load_2d(code_smem + cs * code_tile_bytes + bx * kRowsPerTile * 128, &codes_map, bx * 128,
@@ -1301,6 +1306,24 @@ static int launch_pair_k(const CUtensorMap& map, const CUtensorMap& omap, OneHot
                          : onehot_pair_kernel<K, DIGITS, 1, 4>;
   cudaError_t e = kernel_smem_attr(reinterpret_cast<const void*>(kern));
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(onehot_pair)");
+  if (p.pdl) {
+    // programmatic dependent launch after the layer's encode: barriers, TMEM and the
+    // B image are set up while the encode drains; the producer waits
+    // (griddepcontrol.wait) before its first code tile
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kPairThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, map, omap, p);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernelEx(onehot_pair, PDL)");
+    return LUT_OK;
+  }
   kern<<<grid, kPairThreads, smem, stream>>>(map, omap, p);
   LUT_CHECK_LAUNCH("onehot_pair_kernel");
   return LUT_OK;
@@ -1337,7 +1360,7 @@ static int dispatch_k(int K, const CUtensorMap& map, const CUtensorMap& omap, On
 // codes: (n, code_stride) u8 with code_stride % 16 == 0 (TMA row pitch)
 int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, int K, int M, int digits,
                   const void* image, const float* scales, int scale_mtile, const float* bias, int act, float* out,
-                  int32_t* out_i32, int64_t out_hw, cudaStream_t stream) {
+                  int32_t* out_i32, int64_t out_hw, cudaStream_t stream, int pdl) {
   if (n == 0 || M == 0) return LUT_OK;
   if (!onehot_supported(C, K, M, digits)) return fail(LUT_ERR_CONFIG, "shape not supported by the one-hot gather");
   if (code_stride % 16 != 0 || (reinterpret_cast<uintptr_t>(codes) & 15))
@@ -1368,6 +1391,7 @@ int onehot_gather(const uint8_t* codes, int64_t code_stride, int64_t n, int C, i
   p.out = out;
   p.out_hw = out_hw;
   p.out_i32 = out_i32;
+  p.pdl = pdl;
   {
     const char* dbg = probe_env("LUTGPU_OH_DEBUG");
     p.debug = dbg ? atoi(dbg) : 0;

@@ -55,6 +55,7 @@ struct OneHotParams {
   unsigned long long* tl;     // optional event timeline (LUTGPU_OH_TL=<file>), CTAs 0 and 1 (one pair)
   int sparse;               // 2:4-compressed one-hot A (tcgen05.mma.sp), else dense
   int stage_kb;             // pair kernel, sparse: 128-byte K blocks per A ring stage (1 or 2)
+  int pdl;                  // launched as a programmatic dependent of the layer's encode
   int debug;                // ablation bits (LUTGPU_OH_DEBUG): 1 no epilogue math/stores, 2 no MMA,
                             // 4 no TMEM A stores, 8 MMA only (no A handshake, generators idle)
 };
