@@ -55,6 +55,9 @@ def parse():
                    help="BASELINE configs[i-1]; cfg5 (default) is the headline scaling sweep")
     p.add_argument("--scale-mtile", type=int, default=-1,
                    help="cfg2/cfg4: per-m-tile int8 scales (0 = per table; default: cfg2 128, cfg4 0)")
+    p.add_argument("--cmtile-tensor", action="store_true",
+                   help="cfg2: per-(codebook, m-tile) scales on the tensor cores (dequantized table as 4 digit "
+                        "planes, <= 1e-5) instead of the bitwise CUDA-core f32 sums")
     p.add_argument("--per-table-scales", action="store_true",
                    help="cfg2: one scale per (m-tile) shared by all codebooks instead of BASELINE's per-(c, m-tile)")
     p.add_argument("--no-variants", action="store_true", help="skip the K=64 / fp32 / CUDA-core variant timings")
@@ -638,7 +641,8 @@ def main_stack(args):
     elif wl == "cfg2":
         # BASELINE configs[1]: int8 tables with a per-(c, m-tile) fp32 scale
         mt = 128 if args.scale_mtile < 0 else args.scale_mtile
-        ffn, x = W.ffn_pair(dev, tokens=4096, scale_mtile=mt, per_codebook=not args.per_table_scales)
+        ffn, x = W.ffn_pair(dev, tokens=4096, scale_mtile=mt, per_codebook=not args.per_table_scales,
+                            gather="tensor" if args.cmtile_tensor else "auto")
         fn, rows, unit_rows = (lambda: ffn(x)), 4096, "tokens"
         cpu_objs = (ffn, x, mt, not args.per_table_scales)
     elif wl == "cfg3":
@@ -784,7 +788,7 @@ def main_stack(args):
     # DRAM bytes per step from the committed ncu launch list of this workload's default arguments
     traffic, traffic_src = None, None
     default_table = "f32" if wl in ("cfg1", "cfg3") else "i8"
-    if not args.per_table_scales and args.table == default_table and args.scale_mtile == -1:
+    if not args.per_table_scales and not args.cmtile_tensor and args.table == default_table and args.scale_mtile == -1:
         for rnd in ("r02",):
             try:
                 with open(os.path.join(ROOT, "profiles", rnd, "ncu_traffic_stacks.json")) as f:
@@ -801,7 +805,8 @@ def main_stack(args):
             "config": {"workload": STACKS[wl], "rows_per_step": rows, "cuda_graph": graph is not None,
                        "l2": "256 MB buffer written, then a 256 MB buffer read, between timed steps",
                        "scale_mtile": args.scale_mtile, "table": args.table,
-                       **({"int8_scales": "per (m-tile)" if args.per_table_scales else "per (codebook, m-tile)"}
+                       **({"int8_scales": "per (m-tile)" if args.per_table_scales else
+                           "per (codebook, m-tile), tensor digit planes" if args.cmtile_tensor else "per (codebook, m-tile)"}
                           if wl == "cfg2" else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,

@@ -155,7 +155,8 @@ class LutLayer:
         self.qtable = quantize_table(self.table, self.scale_mtile, self.scale_per_codebook)
         self._deq = None
         self._desc_cache = {}
-        self._images.pop(1, None)
+        for key in [k_ for k_ in self._images if k_ == 1 or isinstance(k_, tuple)]:
+            self._images.pop(key)  # images built from the int8 table (or its dequantized twin)
         self.__dict__.pop("_act_twins", None)
 
     def with_act(self, act) -> "LutLayer":
@@ -190,35 +191,46 @@ class LutLayer:
             self._deq = dequantized_table(self.qtable, self.device)
         return self._deq
 
+    def _dequantized_path(self, integer: bool) -> bool:
+        """Per-(codebook, m-tile) scales: the integer call sums the dequantized entries."""
+        return bool(integer) and self.per_codebook_scales
+
     def uses_tensor_cores(self, integer: bool) -> bool:
         if self.gather == "cuda":
             return False
-        if integer and self.per_codebook_scales:
-            return False  # scales differ per codebook: no single exact integer sum to put on the MMA
+        if self._dequantized_path(integer) and self.gather != "tensor":
+            # scales differ per codebook: no single exact integer sum to put on the MMA; the
+            # default is the bitwise f32 sum, gather="tensor" opts into the digit planes (<= 1e-5)
+            return False
         if self.gather == "auto" and not integer:
             return False
-        digits = 1 if integer else self.f32_digits
+        digits = 1 if (integer and not self.per_codebook_scales) else self.f32_digits
         return load().lut_onehot_image_bytes(self.c, self.k, self.m, digits) > 0
 
     def onehot_image(self, integer: bool) -> torch.Tensor:
-        """Swizzled tcgen05 B image of the table (built once, lut_onehot_prepare_*)."""
-        digits = 1 if integer else self.f32_digits
-        img = self._images.get(digits)
+        """Swizzled tcgen05 B image of the table (built once, lut_onehot_prepare_*): the int8
+        table, or int8 digit planes of the f32 table / of the dequantized per-(codebook,
+        m-tile) table."""
+        deq = self._dequantized_path(integer)
+        digits = 1 if (integer and not deq) else self.f32_digits
+        key = ("deq", digits) if deq else digits
+        img = self._images.get(key)
         if img is None:
             lib = load()
             nbytes = lib.lut_onehot_image_bytes(self.c, self.k, self.m, digits)
             if nbytes == 0:
                 raise ConfigError("shape not supported by the tensor-core gather")
             img = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-            if integer:
+            if integer and not deq:
                 check(lib.lut_onehot_prepare_i8(D.ptr(self.qtable.q), self.c, self.k, self.m, img.data_ptr(),
                                                 D.stream_ptr()), "onehot_prepare_i8")
             else:
+                src = self.dequantized() if deq else self.table
                 err = D.ErrFlag(self.device)
-                check(lib.lut_onehot_prepare_f32(D.ptr(self.table), self.c, self.k, self.m, digits, img.data_ptr(),
+                check(lib.lut_onehot_prepare_f32(D.ptr(src), self.c, self.k, self.m, digits, img.data_ptr(),
                                                  err.p, D.stream_ptr()), "onehot_prepare_f32")
                 check(lib.lut_read_status(err.p, D.stream_ptr()), "onehot_prepare_f32")
-            self._images[digits] = img
+            self._images[key] = img
         return img
 
     def desc(self, integer: bool) -> LayerDesc:
@@ -244,7 +256,7 @@ class LutLayer:
             d.integer = 0
         if self.uses_tensor_cores(integer):
             d.onehot_image = D.ptr(self.onehot_image(integer))
-            d.onehot_digits = 1 if integer else self.f32_digits
+            d.onehot_digits = 1 if (integer and not self.per_codebook_scales) else self.f32_digits
         self._desc_cache[key] = d
         return d
 

@@ -74,3 +74,28 @@ def test_cmtile_not_storable_in_lutn(L):
     dense = L.LutDense(layer)
     with pytest.raises(L.ContainerError):
         L.model_bytes(L.Model([dense]))
+
+
+def test_cmtile_tensor_digit_planes(L):
+    """gather="tensor" opts a per-(codebook, m-tile) layer into the tensor cores: the
+    dequantized table as 4 int8 digit planes (no exact integer sum exists across
+    codebooks), within the north star's fp tolerance (rtol / atol 1e-5) of the bitwise
+    f32 sum; bias + GELU through the same call."""
+    rng = O.make_rng(77)
+    n, c, k, v, m, mt = 900, 24, 16, 32, 3072, 128
+    books = rng.standard_normal((c, k, v)).astype(F32)
+    w = (rng.standard_normal((c * v, m)) * 0.02).astype(F32)
+    bias = rng.standard_normal(m).astype(F32)
+    a = rng.standard_normal((n, c * v)).astype(F32)
+    mk = lambda g: L.LutLayer(cfg=L.PqConfig(v=v, k=k), books=books, weight=w, bias=bias, qat=True, scale_mtile=mt,
+                              scale_per_codebook=True, gather=g)
+    lt, lc = mk("tensor"), mk("auto")
+    assert lt.uses_tensor_cores(True) and not lc.uses_tensor_cores(True)
+    got = L.lut_layer_infer(a, lt, integer=True)
+    ref = L.lut_layer_infer(a, lc, integer=True)
+    q, s = O.quantize_table_cmtile(O.build_table(w, books), mt)
+    want = (O.lut_gather_accumulate_cmtile(O.encode_hard(a, books), q, s, mt) + bias).astype(F32)
+    assert ref.tobytes() == want.tobytes()
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(L.lut_layer_infer(a, lt.with_act("gelu"), integer=True), O.gelu_erf(want),
+                               rtol=1e-5, atol=1e-5)

@@ -11,6 +11,7 @@ for w in cfg1 cfg2 cfg3 cfg4; do
   timeout 300 python bench.py --workload $w --steps 30 --warmup 5 > gpurun_out/r02/stack_$w.json 2>&1; echo "$w rc=$?"
 done
 timeout 300 python bench.py --workload cfg2 --per-table-scales --steps 30 --warmup 5 > gpurun_out/r02/stack_cfg2_mtile.json 2>&1
+timeout 300 python bench.py --workload cfg2 --cmtile-tensor --steps 30 --warmup 5 > gpurun_out/r02/stack_cfg2_cmtile_tensor.json 2>&1
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29541 \
   bench.py --gpus 1 --steps 10 --warmup 3 --no-cpu --no-variants --gather-out --e2e-steps 1 \
   > gpurun_out/r02/bench_torchrun.json 2>&1; echo "torchrun rc=$?"
