@@ -153,6 +153,7 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       prefetch_tmap(&tmap);
+      const uint64_t pol_a = l2_policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t u = blockIdx.x; u < p.nunits; u += gridDim.x) {
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__((2 + 4 * GR) * 32, 1)
           uint8_t* st = smem + stage * kTcStageBytes;
           const float* rec = p.prep + (size_t)c * p.S;
           mbar_arrive_expect_tx(&full[stage], 16384 + NK * 128 + (NK + 4) * 4 + 64);
-          tma_load_2d(st, &tmap, c * 32, (int32_t)(tile * 128), &full[stage]);
+          tma_load_2d_hint(st, &tmap, c * 32, (int32_t)(tile * 128), &full[stage], pol_a);  // A is read once
           bulk_load(st + 16384, rec + prep_base(NK, 32), NK * 128, &full[stage]);   // swizzled tf32 B tile
           bulk_load(st + kAux, rec + NK * 32, (NK + 4) * 4, &full[stage]);           // |p_k|^2, pmax, pad
           bulk_load(st + kAux + 512, rec + prep_base(NK, 32) + NK * 32, 64, &full[stage]);  // 2^-7 max|p_k| (up)

@@ -532,6 +532,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       int64_t rt;
       bool first_b = true;
       bool dep_waited = false;  // the codes come from the preceding encode (programmatic dependent launch)
+      const uint64_t pol_codes = l2_policy_evict_last();  // re-read once per n-tile of the band
       while (walk.next(ntile, rt)) {
         if (ntile != cur_ntile) {
           if (!first_b) {
@@ -559,8 +560,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         }
         mbar_arrive_expect_tx(&code_full[cs], (uint32_t)code_tile_bytes);
         for (int bx = 0; bx < p.code_boxes; ++bx)
-          tma_load_2d(code_smem + cs * code_tile_bytes + bx * kRowsPerTile * 128, &codes_map, bx * 128,
-                      (int32_t)(rt * 2 * kRowsPerTile + rank * kRowsPerTile), &code_full[cs]);
+          tma_load_2d_hint(code_smem + cs * code_tile_bytes + bx * kRowsPerTile * 128, &codes_map, bx * 128,
+                           (int32_t)(rt * 2 * kRowsPerTile + rank * kRowsPerTile), &code_full[cs], pol_codes);
         if (++cs == 2) {
           cs = 0;
           cphase ^= 1;
@@ -809,6 +810,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const uint64_t scale2 = pk_f2(scale0, scale0);
     const bool etr = OH_TRACE(p) && blockIdx.x == 0 && warp == kPEpi0 && lane == 0;
     const bool etl = warp == kPEpi0 && lane == 0;
+    const uint64_t pol_out = l2_policy_evict_first();  // the output is written once and not re-read here
     int epi_unit = 0;
     while (walk.next(ntile, rt)) {
       long long e0 = etr ? clock64() : 0;
@@ -1074,8 +1076,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             named_barrier_sync(6 + 2 * hf, 128);
             if (lane == 0) {
               for (int bx = 0; bx < half_cols / 32; ++bx)
-                tma_store_2d(&out_map, stage_out + hf * half_bytes + bx * (kRowsPerTile * 32 * 4),
-                             m_base + hf * half_cols + bx * 32, (int32_t)row0);
+                tma_store_2d_hint(&out_map, stage_out + hf * half_bytes + bx * (kRowsPerTile * 32 * 4),
+                                  m_base + hf * half_cols + bx * 32, (int32_t)row0, pol_out);
               bulk_commit();
             }
           }
@@ -1085,9 +1087,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           if (etl) TL(16, epi_unit);
           if (lane == 0) {
             for (int bx = 0; bx < half_cols / ib; ++bx)
-              tma_store_2d(&out_map, stage_out + hf * half_bytes + bx * (kRowsPerTile * ib * 4) + sub * 32 * (ib * 4),
-                           m_base + hf * half_cols + bx * ib,
-                           (int32_t)(((OH_DEBUG(p) & 64) ? (row0 & 2047) : row0) + sub * 32));  // 64: L2-resident rows
+              tma_store_2d_hint(&out_map, stage_out + hf * half_bytes + bx * (kRowsPerTile * ib * 4) + sub * 32 * (ib * 4),
+                                m_base + hf * half_cols + bx * ib,
+                                (int32_t)(((OH_DEBUG(p) & 64) ? (row0 & 2047) : row0) + sub * 32), pol_out);  // 64: L2-resident rows
             bulk_commit();
           }
         }

@@ -104,6 +104,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     // ------------------------------------------------ producer (both CTAs)
     if (lane == 0) {
       prefetch_tmap(&codes_map);
+      const uint64_t pol_codes = l2_policy_evict_last();  // re-read once per n-tile of the band
       uint32_t g = 0;  // global stage counter
       int unit = 0;
       int ntile;
@@ -114,9 +115,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         mbar_arrive_expect_tx(&code_full[cs], (uint32_t)code_unit_bytes);
         for (int j = 0; j < 2; ++j)
           for (int bx = 0; bx < p.code_boxes; ++bx)
-            tma_load_2d(code_smem + cs * code_unit_bytes + (j * p.code_boxes + bx) * code_box_bytes, &codes_map,
-                        bx * 128, (int32_t)(rt * 4 * kRowsPerTile + j * 2 * kRowsPerTile + rank * kRowsPerTile),
-                        &code_full[cs]);
+            tma_load_2d_hint(code_smem + cs * code_unit_bytes + (j * p.code_boxes + bx) * code_box_bytes, &codes_map,
+                             bx * 128, (int32_t)(rt * 4 * kRowsPerTile + j * 2 * kRowsPerTile + rank * kRowsPerTile),
+                             &code_full[cs], pol_codes);
         const uint8_t* src = p.b_image + ((size_t)(2 * ntile + (int)rank) * p.nkb) * (64 * kKB);
         for (int st = 0; st < nst; ++st, ++g) {
           const uint32_t bs = g % kSNB;
@@ -343,7 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         } else {
           named_barrier_sync(6 + 2 * a, 128);
           if (grp_leader) {
-            if (mp < p.M) tma_store_2d(&out_map, box, mp, (int32_t)row0);
+            if (mp < p.M) tma_store_2d_hint(&out_map, box, mp, (int32_t)row0, l2_policy_evict_first());
             bulk_commit();
           }
         }
