@@ -70,4 +70,5 @@ def timed(fn, name, steps=30):
 timed(lambda: None if torch.zeros(1, device=dev).add_(1) is None else None, "tiny torch kernel (floor)")
 timed(enc, "encode only")
 timed(gat, "gather only (codes in L2?)")
+timed(lambda: (enc(), gat()), "encode + gather, no PDL")
 timed(both, "layer (encode + PDL gather)")
