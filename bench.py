@@ -168,6 +168,8 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.samples = []
+        self.power_w = []
+        self.mem_mhz = []
         self.reasons = set()
         self.max_mhz = None
         self._stop = threading.Event()
@@ -191,13 +193,18 @@ class ClockSampler:
                 while not self._stop.is_set():
                     try:
                         self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                        try:
+                            self.power_w.append(N.nvmlDeviceGetPowerUsage(h) / 1e3)
+                            self.mem_mhz.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_MEM))
+                        except Exception:
+                            pass
                         r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
                         for nm, bit in names.items():
                             if r & bit:
                                 self.reasons.add(nm)
                     except Exception:
                         pass
-                    self._stop.wait(0.02)
+                    self._stop.wait(0.002)
 
             self._t = threading.Thread(target=run, daemon=True)
             self._t.start()
@@ -212,7 +219,11 @@ class ClockSampler:
 
     def summary(self):
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "sm_mhz_min": min(self.samples) if self.samples else None,
+                "sm_mhz_hist": {str(k_): self.samples.count(k_) for k_ in sorted(set(self.samples))},
+                "mem_mhz": statistics.median(self.mem_mhz) if self.mem_mhz else None,
+                "power_w_max": max(self.power_w) if self.power_w else None}
 
 
 # ------------------------------------------------------------- GPU side
