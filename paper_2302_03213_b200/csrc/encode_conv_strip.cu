@@ -324,10 +324,9 @@ int launch_conv_strip(const float* x, int batch, int cin, int h, int w, int stri
   if (hw_out <= 0 || hw_out > 4096) return LUT_OK;
   ConvStripParams p;
   const int P = (wo & 3) == 0 ? 4 : 2;
-#ifndef CS_UNIT_PX
-#define CS_UNIT_PX 1024
-#endif
-  p.ib = hw_out >= CS_UNIT_PX ? 1 : (CS_UNIT_PX / hw_out < batch ? CS_UNIT_PX / hw_out : batch);
+  // ~1024 output pixels per unit (512 and 256 measured slower: more per-unit staging / syncs)
+  constexpr int kUnitPx = 1024;
+  p.ib = hw_out >= kUnitPx ? 1 : (kUnitPx / hw_out < batch ? kUnitPx / hw_out : batch);
   p.plane_floats = (uint32_t)(h * w);
   p.slot_bytes = (uint32_t)(((int64_t)p.ib * kCsWarps * plane_bytes + 127) & ~(int64_t)127);
   const size_t smem = 2 * (size_t)p.slot_bytes + kCsWarps * kCsRec * 4 + (((size_t)p.ib * hw_out * 8 + 15) & ~(size_t)15) +
